@@ -1,0 +1,302 @@
+/*
+ * pathrec_gpu.h — C ABI of the B200-native Path Sorting + Path Recycling engine.
+ *
+ * This is the drop-in boundary for the reference's hot path (arXiv 2110.00085,
+ * reference `pathrec`, /root/reference/proj).  The reference's C++ calls that the
+ * recycling loop is made of, and the entry point here that replaces each one:
+ *
+ *   pathrec::render(scene, {keep_paths})      transport.hpp:174, transport.cpp:405-454
+ *        -> prc_gpu_render                      (K1 trace + K4 fresh evaluation)
+ *   pathrec::sort_by_size(store)              pathstore.hpp:28, pathstore.cpp:261-267
+ *        -> prc_gpu_sort_by_size                (K2 stable counting sort by B)
+ *   pathrec::evaluate_store(scene, store, t, opt)   pathstore.hpp:64, pathstore.cpp:315-368
+ *        -> prc_gpu_evaluate                    (K3 prep, K4 forward, K5 gradient)
+ *   pathrec::recycled_render(...)             pathstore.hpp:68, pathstore.cpp:370-375
+ *        -> prc_gpu_evaluate with want_grad = 0
+ *   pathrec::grad_forward(...)                gradient.hpp:40, gradient.cpp:111-128
+ *        -> prc_gpu_evaluate with want_grad = 1
+ *   pathrec::reconstruct / adam_step / loss   inverse.hpp:274-295, inverse.cpp:11-67,154-263
+ *        -> prc_gpu_opt_* (device-resident Algorithm 2 iteration) and prc_gpu_reconstruct
+ *   pathrec::save_store / load_store (PSTR v1) pathstore.cpp:410-516
+ *        -> prc_gpu_store_export_pstr / prc_gpu_store_import_pstr
+ *
+ * Conventions follow the reference C ABI (include/pathrec.h:11-23, src/capi.cpp:17-32):
+ * opaque handles, int error codes, a thread-local last-error string, no exceptions
+ * across the boundary, caller-owned option structs, one *_free per handle.
+ * Every entry point is synchronous.  Plain pointers and sizes only; no torch types.
+ */
+#ifndef PATHREC_GPU_H
+#define PATHREC_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Error codes: same values as the reference enum (pathrec.h:13-19) plus CUDA. */
+enum {
+    PRC_OK = 0,
+    PRC_ERR_CONFIG = 1,  /* bad option values, malformed scene */
+    PRC_ERR_IO = 2,      /* missing or unreadable/unwritable files */
+    PRC_ERR_NUMERIC = 3, /* non-finite results, aborted optimization */
+    PRC_ERR_INVALID = 4, /* null handles, out-of-range indices */
+    PRC_ERR_CUDA = 5     /* device / driver / NCCL failure (no CPU fallback exists) */
+};
+
+/* ---------------------------------------------------------------------------
+ * Scene description (value mirror of pathrec::Scene, scene.hpp:26-107).
+ * All arrays are borrowed for the duration of the call that receives them.
+ * ------------------------------------------------------------------------- */
+
+typedef struct {
+    double x, y, z;
+} prc_vec3;
+
+/* PhaseFunction::Kind (phase.hpp:19) */
+enum { PRC_PHASE_HG = 0, PRC_PHASE_RAYLEIGH = 1 };
+/* Surface::Kind (scene.hpp:79), Brdf::Kind (brdf.hpp:41) */
+enum { PRC_SURF_SPHERE = 0, PRC_SURF_FACE = 1 };
+enum { PRC_BRDF_DIFFUSE = 0, PRC_BRDF_PHONG = 1 };
+/* LightSource::Kind (scene.hpp:57) */
+enum { PRC_LIGHT_SUN = 0, PRC_LIGHT_POINT = 1 };
+
+/* ParticleSpecies (scene.hpp:26-32).  All species share one grid geometry. */
+typedef struct {
+    const double* extinction; /* voxel_count values, x-fastest (grid.hpp:15-24) */
+    double albedo;
+    int phase_kind;           /* PRC_PHASE_* */
+    double g;                 /* HG asymmetry (ignored for Rayleigh) */
+    int unknown;              /* tomography target (at most one, scene.cpp:145-147) */
+} prc_species_desc;
+
+/* Surface + Sphere + BoxFace + Brdf (scene.hpp:63-86, brdf.hpp:12-63) */
+typedef struct {
+    int kind;                 /* PRC_SURF_* */
+    prc_vec3 center;          /* sphere */
+    double radius;
+    int axis;                 /* face: plane axis 0..2 */
+    double coord;             /* face: plane coordinate */
+    double lo[2], hi[2];      /* face: extents on the other two axes, in axis order */
+    double normal_sign;       /* face: +1 normal toward +axis */
+    int brdf_kind;            /* PRC_BRDF_* */
+    double albedo;            /* diffuse albedo */
+    double kappa_s, gamma;    /* Phong lobe */
+    int target;               /* reflectometry unknown surface (Phong) */
+} prc_surface_desc;
+
+/* LightSource (scene.hpp:56-61) */
+typedef struct {
+    int kind;                 /* PRC_LIGHT_* */
+    prc_vec3 position;        /* point light */
+    prc_vec3 direction;       /* sun propagation direction */
+    double radiance;
+} prc_light_desc;
+
+/* Detector (scene.hpp:34-54); the frame is derived as Detector::finalize (scene.cpp:8-14). */
+typedef struct {
+    prc_vec3 position;
+    prc_vec3 direction;
+    prc_vec3 up;
+    int rows, cols;
+    double fov;               /* full horizontal field of view [rad] */
+} prc_detector_desc;
+
+typedef struct {
+    prc_vec3 bounds_min, bounds_max;   /* Scene::bounds */
+    int dims[3];                       /* GridGeometry (ignored when n_species == 0) */
+    prc_vec3 grid_origin, voxel_size;
+    int n_species;
+    const prc_species_desc* species;
+    int n_surfaces;
+    const prc_surface_desc* surfaces;
+    prc_light_desc light;
+    int n_detectors;
+    const prc_detector_desc* detectors;
+} prc_scene_desc;
+
+/* ParamSet (transport.hpp:63-67): the unknowns decoupled from the scene.
+ * beta: unknown species' extinction per voxel (n_beta == voxel_count) or NULL to
+ * use the scene's values.  species_beta (extension for per-type work, config (c)):
+ * optional array of n_species pointers overriding every species; NULL entries keep
+ * the scene's (or `beta`'s) values. */
+typedef struct {
+    const double* beta;
+    uint64_t n_beta;
+    double kappa_s, gamma;
+    const double* const* species_beta;
+} prc_gpu_params;
+
+/* ---------------------------------------------------------------------------
+ * Context: one per process; owns the device(s), streams, the scene copy and the
+ * NCCL communicator.  Paths are sharded over ranks by contiguous stream ranges.
+ * ------------------------------------------------------------------------- */
+
+typedef struct prc_gpu_ctx prc_gpu_ctx;
+typedef struct prc_gpu_store prc_gpu_store;
+
+const char* prc_gpu_version(void);
+const char* prc_gpu_last_error(void);
+
+/* Single-GPU context on CUDA device `device`. */
+int prc_gpu_ctx_create(int device, prc_gpu_ctx** out);
+/* One process per GPU: joins an NCCL communicator of `world` ranks.  nccl_id is the
+ * 128-byte ncclUniqueId produced by prc_gpu_nccl_unique_id on rank 0 and broadcast
+ * by the caller (e.g. through torch.distributed). */
+int prc_gpu_nccl_unique_id(void* out128);
+int prc_gpu_ctx_create_rank(int device, int rank, int world, const void* nccl_id,
+                            prc_gpu_ctx** out);
+void prc_gpu_ctx_destroy(prc_gpu_ctx* ctx);
+int prc_gpu_ctx_rank(const prc_gpu_ctx* ctx, int* rank, int* world);
+
+/* Uploads (and validates, finalizes) the scene; replaces any previous scene and
+ * frees every store built against it. */
+int prc_gpu_scene_upload(prc_gpu_ctx* ctx, const prc_scene_desc* scene);
+int prc_gpu_scene_voxel_count(const prc_gpu_ctx* ctx, uint64_t* out);
+/* Total image pixels over detectors (images are concatenated detector-major). */
+int prc_gpu_scene_pixel_count(const prc_gpu_ctx* ctx, uint64_t* out);
+
+/* ---------------------------------------------------------------------------
+ * Path generation (K1) — pathrec::render (transport.cpp:405-454).
+ * ------------------------------------------------------------------------- */
+
+typedef struct {
+    uint64_t n_paths;         /* global path count (all ranks) */
+    uint64_t seed;
+    int max_bounces;          /* <= 0: default 500 */
+    int max_scatter_events;   /* < 0: unlimited (RenderOptions, transport.hpp:154-161) */
+} prc_gpu_render_opts;
+
+/* Traces n_paths paths under `params` (NULL: scene values; bind_params semantics,
+ * inverse.cpp:144-150) and evaluates them at that point (the fresh image).
+ * images_out: host buffer of pixel_count doubles, normalised by 1/N (may be NULL).
+ * store_out: non-NULL keeps the path store (keep_paths). */
+int prc_gpu_render(prc_gpu_ctx* ctx, const prc_gpu_render_opts* opts, const prc_gpu_params* params,
+                   double* images_out, uint64_t* truncated_out, prc_gpu_store** store_out);
+
+/* K2: stable sort by ascending B (pathstore.cpp:261-267); re-lays the device store
+ * out bucket-major so a warp of consecutive paths reads coalesced records. */
+int prc_gpu_sort_by_size(prc_gpu_ctx* ctx, prc_gpu_store* store);
+
+typedef struct {
+    uint64_t n_paths;          /* paths in this rank's shard */
+    uint64_t n_paths_global;   /* normalisation count */
+    uint64_t stream_base;      /* first global stream id of this shard */
+    uint64_t segments;         /* S = sum of B (dead final segments included) */
+    uint64_t vertices;         /* sum of (B + 1) */
+    uint64_t interaction_vertices; /* sum of (B - 1) */
+    uint64_t truncated;
+    uint64_t seed, generation;
+    int sorted;
+    int max_size;              /* max B */
+    uint64_t device_bytes;     /* device memory held by the store */
+} prc_gpu_store_info;
+
+int prc_gpu_store_info_get(const prc_gpu_store* store, prc_gpu_store_info* out);
+/* Stream ids in storage order (PathStore::records[i].stream). */
+int prc_gpu_store_streams(const prc_gpu_store* store, uint64_t* out);
+/* Path sizes B in storage order. */
+int prc_gpu_store_sizes(const prc_gpu_store* store, uint32_t* out);
+/* PSTR v1 interchange (pathstore.cpp:410-516).  Export materialises every span and
+ * event on the device.  Import accepts reference-written files. */
+int prc_gpu_store_export_pstr(prc_gpu_ctx* ctx, const prc_gpu_store* store, const char* path);
+int prc_gpu_store_import_pstr(prc_gpu_ctx* ctx, const char* path, prc_gpu_store** out);
+int prc_gpu_store_set_generation(prc_gpu_store* store, uint64_t generation);
+void prc_gpu_store_free(prc_gpu_store* store);
+
+/* ---------------------------------------------------------------------------
+ * Recycled evaluation (K3/K4/K5) — pathrec::evaluate_store (pathstore.cpp:315-368).
+ * ------------------------------------------------------------------------- */
+
+enum {
+    PRC_EVAL_NORMALIZE = 1,     /* divide by the global record count (default on) */
+    PRC_EVAL_WANT_GRAD = 2,
+    PRC_EVAL_LEGACY_SCORE = 4,  /* pathstore.cpp:98-101 */
+    PRC_EVAL_SELF_NORMALIZE = 8,/* rejected: PRC_ERR_CONFIG (not on the recycling loop) */
+    PRC_EVAL_PER_SPECIES = 16   /* per-type gradients: grad_out holds n_species x V */
+};
+
+typedef struct {
+    int flags;                    /* PRC_EVAL_* */
+    const double* pixel_weights;  /* host, pixel_count doubles (residuals) or NULL = 1 */
+} prc_gpu_eval_opts;
+
+typedef struct {
+    double* images;      /* host, pixel_count doubles, or NULL */
+    double* grad_beta;   /* host, V doubles (or n_species*V with PER_SPECIES), or NULL */
+    double grad_kappa, grad_gamma;
+    uint64_t clamp_events;
+    double mean_correction;
+} prc_gpu_eval_result;
+
+int prc_gpu_evaluate(prc_gpu_ctx* ctx, const prc_gpu_store* store, const prc_gpu_params* params,
+                     const prc_gpu_eval_opts* opts, prc_gpu_eval_result* result);
+
+/* ---------------------------------------------------------------------------
+ * Device-resident Algorithm 2 (inverse.cpp:154-263): the recycled iteration
+ * K3 -> K4 -> allreduce(images) -> loss/residual -> K5 -> allreduce(grad) -> K6 ADAM,
+ * with parameters, moments and the ground truth resident in HBM.
+ * ------------------------------------------------------------------------- */
+
+typedef struct {
+    double alpha, eta1, eta2, eps_guard;  /* AdamConfig (inverse.hpp:11-21) */
+    int project_nonneg;
+    const double* step_scale;             /* n_step_scale multipliers or NULL */
+    int n_step_scale;
+} prc_gpu_adam_config;
+
+/* gt_images: host, pixel_count doubles.  initial: starting unknowns. */
+int prc_gpu_opt_init(prc_gpu_ctx* ctx, const prc_gpu_params* initial, const double* gt_images,
+                     const prc_gpu_adam_config* adam);
+/* One recycled iteration over `store`; loss_out receives 0.5*||F - gt||^2. */
+int prc_gpu_opt_step(prc_gpu_ctx* ctx, const prc_gpu_store* store, double* loss_out);
+/* Copies the current unknowns out (beta: V doubles or NULL). */
+int prc_gpu_opt_params(prc_gpu_ctx* ctx, double* beta_out, double* kappa_s, double* gamma);
+/* Current device forward images (pixel_count doubles) of the last step. */
+int prc_gpu_opt_images(prc_gpu_ctx* ctx, double* images_out);
+
+typedef struct {
+    uint64_t seed;
+    uint64_t n_paths;
+    int max_bounces;
+    int recycle_period;       /* N_r (Schedule::recycle_period) */
+    int max_iterations;
+} prc_gpu_reconstruct_opts;
+
+/* Algorithm 2 with a single stage: resample + sort every N_r iterations (seed
+ * schedule of inverse.cpp:193), otherwise recycle.  loss_history: max_iterations
+ * doubles or NULL.  sampling_phases_out may be NULL. */
+int prc_gpu_reconstruct(prc_gpu_ctx* ctx, const prc_gpu_params* initial, const double* gt_images,
+                        const prc_gpu_adam_config* adam, const prc_gpu_reconstruct_opts* opts,
+                        double* loss_history, uint64_t* sampling_phases_out);
+
+/* ---------------------------------------------------------------------------
+ * Timing and device-side diagnostics (used by tests and bench; not on the API path).
+ * ------------------------------------------------------------------------- */
+
+/* Milliseconds of the most recent evaluate / opt_step kernels, measured with CUDA
+ * events on the launching stream: [0] prep, [1] forward (K4), [2] image allreduce +
+ * loss, [3] gradient (K5), [4] grad allreduce + ADAM, [5] total. */
+int prc_gpu_last_timings(const prc_gpu_ctx* ctx, double* ms6);
+/* Number of kernels this library launched since ctx creation. */
+int prc_gpu_kernel_launches(const prc_gpu_ctx* ctx, uint64_t* out);
+
+/* Philox4x32-10 words from the device generator (rng.hpp:11-61): n words of stream. */
+int prc_gpu_debug_philox(prc_gpu_ctx* ctx, uint64_t seed, uint64_t stream, uint64_t n,
+                         uint32_t* out);
+/* Device fp64 DDA (traverse.hpp:45-116) over n rays against the uploaded grid.
+ * rays: n x 7 doubles (origin xyz, direction xyz, max_distance).
+ * counts_out[n]; when voxels_out/lengths_out are non-NULL they receive the spans of
+ * all rays concatenated (capacity `cap`). */
+int prc_gpu_debug_walk(prc_gpu_ctx* ctx, uint64_t n, const double* rays, uint32_t* counts_out,
+                       uint32_t* voxels_out, double* lengths_out, uint64_t cap);
+/* Device Detector::pixel_of (scene.cpp:16-28) for n points against detector det. */
+int prc_gpu_debug_pixel_of(prc_gpu_ctx* ctx, int det, uint64_t n, const double* points,
+                           int32_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PATHREC_GPU_H */

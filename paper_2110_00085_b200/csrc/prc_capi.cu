@@ -1,0 +1,1598 @@
+// prc_capi.cu — host runtime and C ABI (include/pathrec_gpu.h) of the B200 engine.
+//
+// The context owns one CUDA device, one stream, the finalized scene and (for
+// world > 1) an NCCL communicator; a path store is a device-resident SoA shard of
+// contiguous stream ids [stream_base, stream_base + n).  Reference counterparts:
+// render (transport.cpp:405-454), sort_by_size (pathstore.cpp:261-267),
+// evaluate_store (pathstore.cpp:315-368), grad_forward (gradient.cpp:111-128),
+// reconstruct / adam_step / loss (inverse.cpp:11-67, 154-263), PSTR v1
+// (pathstore.cpp:410-516), C-ABI conventions (capi.cpp:17-32).
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/pathrec_gpu.h"
+#include "prc_kernels.cuh"
+
+#define PRC_EXPORT extern "C" __attribute__((visibility("default")))
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct Err : std::runtime_error {
+    int code;
+    Err(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define CK(x)                                                                            \
+    do {                                                                                 \
+        cudaError_t _e = (x);                                                            \
+        if (_e != cudaSuccess)                                                           \
+            throw Err(PRC_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(_e));    \
+    } while (0)
+#define NK(x)                                                                            \
+    do {                                                                                 \
+        ncclResult_t _r = (x);                                                           \
+        if (_r != ncclSuccess)                                                           \
+            throw Err(PRC_ERR_CUDA, std::string(#x) + ": " + ncclGetErrorString(_r));    \
+    } while (0)
+
+template <class T>
+struct DBuf {  // owning device buffer
+    T* p = nullptr;
+    size_t n = 0;
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    ~DBuf() { reset(); }
+    void reset() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    void alloc(size_t count) {
+        if (count == n && p) return;
+        reset();
+        if (count == 0) return;
+        CK(cudaMalloc(&p, count * sizeof(T)));
+        n = count;
+    }
+    void grow(size_t count) {
+        if (count > n) alloc(count);
+    }
+    size_t bytes() const { return n * sizeof(T); }
+    void swap(DBuf& o) {
+        std::swap(p, o.p);
+        std::swap(n, o.n);
+    }
+};
+
+// --------------------------------------------------------------- host fp64 vector ops
+// Same operation order as vec3.hpp (compiled with -ffp-contract=off).
+struct H3 {
+    double x, y, z;
+};
+H3 h3(const prc_vec3& v) { return {v.x, v.y, v.z}; }
+H3 hsub(H3 a, H3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+double hdot(H3 a, H3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+double hnorm(H3 a) { return std::sqrt(a.x * a.x + a.y * a.y + a.z * a.z); }
+H3 hnormalized(H3 a) {
+    const double n = hnorm(a);
+    return {a.x / n, a.y / n, a.z / n};
+}
+H3 hcross(H3 a, H3 b) { return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x}; }
+void put3(double* d, H3 v) {
+    d[0] = v.x;
+    d[1] = v.y;
+    d[2] = v.z;
+}
+
+}  // namespace
+
+struct prc_gpu_store;
+
+struct prc_gpu_ctx {
+    int device = 0, rank = 0, world = 1;
+    ncclComm_t comm = nullptr;
+    cudaStream_t stream = nullptr;
+    unsigned long long launches = 0;
+    // scene
+    bool have_scene = false;
+    DScene dsc{};
+    long long V = 0, n_pix = 0;
+    std::vector<double> host_sp;  // n_species x V (scene values)
+    DBuf<double> scene_sp;        // device copy
+    std::vector<prc_surface_desc> surfaces;
+    double scene_kappa = 0.0, scene_gamma = 0.0;
+    // evaluation scratch
+    DBuf<float> sp_t, bt_tot, dbeta;
+    DBuf<double> param_beta, species_t, trace_sp, images, weights, g_span, g_vert, g_out, phong,
+        g_phong, loss;
+    DBuf<unsigned long long> clamps, u64tmp_a, u64tmp_b, n_trunc;
+    DBuf<uint32_t> u32tmp;
+    DBuf<int> err;
+    void* cub_tmp = nullptr;
+    size_t cub_bytes = 0;
+    // device-resident optimizer (Algorithm 2)
+    bool opt_ready = false;
+    int opt_mode = 0;  // 0 tomography, 1 Phong
+    DBuf<double> opt_x, opt_m1, opt_m2, opt_gt, opt_step_scale;
+    long long opt_n = 0;
+    int64_t opt_t = 0;
+    prc_gpu_adam_config adam{};
+    int n_step_scale = 0;
+    // timing
+    cudaEvent_t ev[6] = {};
+    double last_ms[6] = {};
+    ~prc_gpu_ctx() {
+        if (cub_tmp) cudaFree(cub_tmp);
+        for (auto& e : ev)
+            if (e) cudaEventDestroy(e);
+        if (comm) ncclCommDestroy(comm);
+        if (stream) cudaStreamDestroy(stream);
+    }
+    void sync() { CK(cudaStreamSynchronize(stream)); }
+    void check_scene() const {
+        if (!have_scene) throw Err(PRC_ERR_INVALID, "no scene uploaded");
+    }
+    void allreduce(double* buf, size_t count) {
+        if (world > 1 && count > 0)
+            NK(ncclAllReduce(buf, buf, count, ncclFloat64, ncclSum, comm, stream));
+    }
+    void allreduce_u64(unsigned long long* buf, size_t count) {
+        if (world > 1 && count > 0)
+            NK(ncclAllReduce(buf, buf, count, ncclUint64, ncclSum, comm, stream));
+    }
+};
+
+struct prc_gpu_store {
+    prc_gpu_ctx* ctx = nullptr;
+    unsigned long long n = 0, n_global = 0, stream_base = 0, seed = 0, generation = 0;
+    bool sorted = false;
+    int max_B = 0;
+    DBuf<uint32_t> B, stride;
+    DBuf<unsigned long long> stream, rec_base, iv_base;
+    DBuf<uint8_t> trunc;
+    DBuf<double> px, py, pz, dx, dy, dz, tt, ct;
+    DBuf<int32_t> vox;
+    DBuf<uint32_t> meta;
+    unsigned long long n_rec = 0, n_iv = 0;
+    DBuf<float> ev_val;
+    DBuf<int32_t> ev_pix;
+    DBuf<double> br_tot64;
+    DBuf<float> sp_ref, br_tot;
+    std::vector<double> ref_beta;
+    double ref_kappa = 0.0, ref_gamma = 0.0;
+    unsigned long long segments = 0, truncated = 0;
+
+    StoreView view() {
+        StoreView v{};
+        v.n = n;
+        v.B = B.p;
+        v.rec_base = rec_base.p;
+        v.stride = stride.p;
+        v.iv_base = iv_base.p;
+        v.px = px.p;
+        v.py = py.p;
+        v.pz = pz.p;
+        v.dx = dx.p;
+        v.dy = dy.p;
+        v.dz = dz.p;
+        v.tt = tt.p;
+        v.ct = ct.p;
+        v.vox = vox.p;
+        v.meta = meta.p;
+        v.n_iv = n_iv;
+        v.ev_val = ev_val.p;
+        v.ev_pix = ev_pix.p;
+        return v;
+    }
+    void alloc_records(unsigned long long nr) {
+        n_rec = nr;
+        px.alloc(nr);
+        py.alloc(nr);
+        pz.alloc(nr);
+        dx.alloc(nr);
+        dy.alloc(nr);
+        dz.alloc(nr);
+        tt.alloc(nr);
+        ct.alloc(nr);
+        vox.alloc(nr);
+        meta.alloc(nr);
+    }
+    RecordsOut rec_out() {
+        return RecordsOut{px.p, py.p, pz.p, dx.p, dy.p, dz.p, tt.p, ct.p, vox.p, meta.p};
+    }
+    unsigned long long device_bytes() const {
+        return B.bytes() + stride.bytes() + stream.bytes() + rec_base.bytes() + iv_base.bytes() +
+               trunc.bytes() + px.bytes() * 8 + vox.bytes() + meta.bytes() + ev_val.bytes() +
+               ev_pix.bytes() + br_tot64.bytes() + sp_ref.bytes() + br_tot.bytes();
+    }
+};
+
+namespace {
+
+int fail(int code, const std::string& m) {
+    g_last_error = m;
+    return code;
+}
+
+int classify(const std::exception& e) {
+    if (auto* x = dynamic_cast<const Err*>(&e)) return x->code;
+    if (dynamic_cast<const std::bad_alloc*>(&e)) return PRC_ERR_CUDA;
+    return PRC_ERR_CONFIG;
+}
+
+#define ABI_TRY try {
+#define ABI_CATCH                               \
+    }                                           \
+    catch (const std::exception& e) {           \
+        return fail(classify(e), e.what());     \
+    }                                           \
+    return PRC_OK;
+
+void begin(prc_gpu_ctx* c) { CK(cudaSetDevice(c->device)); }
+
+// ----------------------------------------------------------------------- scene upload
+void upload_scene(prc_gpu_ctx* c, const prc_scene_desc* d) {
+    if (d->n_species < 0 || d->n_species > PRC_MAX_SPECIES)
+        throw Err(PRC_ERR_CONFIG, "scene: species count outside 0..16");
+    if (d->n_surfaces < 0 || d->n_surfaces > PRC_MAX_SURF)
+        throw Err(PRC_ERR_CONFIG, "scene: at most 32 surfaces supported");
+    if (d->n_detectors < 1 || d->n_detectors > PRC_MAX_DET)
+        throw Err(PRC_ERR_CONFIG, "scene: detector count outside 1..32");
+    DScene s{};
+    s.bmin[0] = d->bounds_min.x;
+    s.bmin[1] = d->bounds_min.y;
+    s.bmin[2] = d->bounds_min.z;
+    s.bmax[0] = d->bounds_max.x;
+    s.bmax[1] = d->bounds_max.y;
+    s.bmax[2] = d->bounds_max.z;
+    s.has_medium = d->n_species > 0;
+    s.n_species = d->n_species;
+    long long V = 0;
+    if (s.has_medium) {
+        for (int a = 0; a < 3; ++a) {
+            if (d->dims[a] <= 0) throw Err(PRC_ERR_CONFIG, "scene: grid dims must be positive");
+            s.dims[a] = d->dims[a];
+        }
+        s.gorg[0] = d->grid_origin.x;
+        s.gorg[1] = d->grid_origin.y;
+        s.gorg[2] = d->grid_origin.z;
+        s.vs[0] = d->voxel_size.x;
+        s.vs[1] = d->voxel_size.y;
+        s.vs[2] = d->voxel_size.z;
+        for (int a = 0; a < 3; ++a) s.gmax[a] = s.gorg[a] + s.dims[a] * s.vs[a];  // grid.hpp:27-30
+        V = (long long)s.dims[0] * s.dims[1] * s.dims[2];
+    }
+    s.V = V;
+    s.unknown = -1;
+    std::vector<double> sp((size_t)d->n_species * (size_t)V);
+    for (int j = 0; j < d->n_species; ++j) {
+        const prc_species_desc& q = d->species[j];
+        if (!q.extinction) throw Err(PRC_ERR_CONFIG, "scene: species extinction is null");
+        std::memcpy(sp.data() + (size_t)j * V, q.extinction, (size_t)V * sizeof(double));
+        s.sp[j].albedo = q.albedo;
+        s.sp[j].g = q.g;
+        s.sp[j].kind = q.phase_kind == PRC_PHASE_RAYLEIGH ? 1 : 0;
+        s.sp[j].unknown = q.unknown;
+        if (q.unknown) {
+            if (s.unknown >= 0) throw Err(PRC_ERR_CONFIG, "more than one unknown species");
+            s.unknown = j;
+        }
+        if (s.sp[j].kind == 0 && std::abs(q.g) >= 1.0) throw Err(PRC_ERR_CONFIG, "|g| must be < 1");
+    }
+    s.n_surf = d->n_surfaces;
+    s.target = -1;
+    c->scene_kappa = c->scene_gamma = 0.0;
+    for (int k = 0; k < d->n_surfaces; ++k) {
+        const prc_surface_desc& q = d->surfaces[k];
+        DSurf& f = s.surf[k];
+        f.kind = q.kind == PRC_SURF_FACE ? 1 : 0;
+        f.axis = q.axis;
+        f.brdf_kind = q.brdf_kind == PRC_BRDF_PHONG ? 1 : 0;
+        f.target = q.target;
+        put3(f.c, h3(q.center));
+        f.radius = q.radius;
+        f.coord = q.coord;
+        f.lo[0] = q.lo[0];
+        f.lo[1] = q.lo[1];
+        f.hi[0] = q.hi[0];
+        f.hi[1] = q.hi[1];
+        f.normal_sign = q.normal_sign;
+        f.albedo = q.albedo;
+        f.kappa = q.kappa_s;
+        f.gamma = q.gamma;
+        if (f.kind == 1 && (q.axis < 0 || q.axis > 2)) throw Err(PRC_ERR_CONFIG, "face axis outside 0..2");
+        if (q.target) {
+            if (s.target >= 0) throw Err(PRC_ERR_CONFIG, "more than one target surface");
+            if (f.brdf_kind != 1) throw Err(PRC_ERR_CONFIG, "target surface must carry a Phong lobe");
+            s.target = k;
+            c->scene_kappa = q.kappa_s;
+            c->scene_gamma = q.gamma;
+        }
+    }
+    s.light_kind = d->light.kind == PRC_LIGHT_SUN ? 0 : 1;
+    put3(s.light_pos, h3(d->light.position));
+    H3 ld = h3(d->light.direction);
+    if (s.light_kind == 0) ld = hnormalized(ld);  // Scene::finalize, scene.cpp:71-74
+    put3(s.light_dir, ld);
+    s.radiance = d->light.radiance;
+    // emission_prefactor, transport.cpp:347-351
+    s.prefactor = s.light_kind == 1 ? PRC_FOUR_PI * s.radiance
+                                    : (s.bmax[0] - s.bmin[0]) * (s.bmax[1] - s.bmin[1]) * s.radiance;
+    s.n_det = d->n_detectors;
+    long long off = 0;
+    for (int k = 0; k < d->n_detectors; ++k) {  // Detector::finalize, scene.cpp:8-14
+        const prc_detector_desc& q = d->detectors[k];
+        if (q.rows <= 0 || q.cols <= 0) throw Err(PRC_ERR_CONFIG, "detector: non-positive pixel grid");
+        DDet& t = s.det[k];
+        const H3 dir = hnormalized(h3(q.direction));
+        const H3 right = hnormalized(hcross(dir, h3(q.up)));
+        const H3 up = hcross(right, dir);
+        put3(t.pos, h3(q.position));
+        put3(t.dir, dir);
+        put3(t.right, right);
+        put3(t.up, up);
+        t.hw = std::tan(0.5 * q.fov);
+        t.hh = t.hw * static_cast<double>(q.rows) / static_cast<double>(q.cols);
+        t.rows = q.rows;
+        t.cols = q.cols;
+        t.img_off = off;
+        off += (long long)q.rows * q.cols;
+    }
+    s.n_pix = off;
+    c->dsc = s;
+    c->V = V;
+    c->n_pix = off;
+    c->host_sp.swap(sp);
+    c->surfaces.assign(d->surfaces, d->surfaces + d->n_surfaces);
+    c->scene_sp.alloc(c->host_sp.size());
+    if (!c->host_sp.empty())
+        CK(cudaMemcpy(c->scene_sp.p, c->host_sp.data(), c->host_sp.size() * sizeof(double),
+                      cudaMemcpyHostToDevice));
+    const size_t nsV = (size_t)std::max(1, d->n_species) * (size_t)std::max<long long>(V, 1);
+    c->sp_t.alloc(nsV);
+    c->bt_tot.alloc((size_t)std::max<long long>(V, 1));
+    c->dbeta.alloc((size_t)std::max<long long>(V, 1));
+    c->param_beta.alloc((size_t)std::max<long long>(V, 1));
+    c->species_t.alloc(nsV);
+    c->trace_sp.alloc(nsV);
+    c->images.alloc((size_t)off);
+    c->weights.alloc((size_t)off);
+    c->g_span.alloc((size_t)std::max<long long>(V, 1));
+    c->g_vert.alloc(nsV);
+    c->g_out.alloc(nsV);
+    c->phong.alloc(2);
+    c->g_phong.alloc(2);
+    c->loss.alloc(1);
+    c->clamps.alloc(1);
+    c->n_trunc.alloc(1);
+    c->err.alloc(1);
+    c->have_scene = true;
+    c->opt_ready = false;
+}
+
+// Species source pointers + Phong values for the evaluated parameters.
+struct Resolved {
+    const double* src[PRC_MAX_SPECIES] = {};
+    double kappa = 0.0, gamma = 0.0;
+};
+
+Resolved resolve_params(prc_gpu_ctx* c, const prc_gpu_params* p, const prc_gpu_store* ref_store) {
+    Resolved r;
+    const DScene& s = c->dsc;
+    for (int j = 0; j < s.n_species; ++j) r.src[j] = c->scene_sp.p + (size_t)j * c->V;
+    r.kappa = c->scene_kappa;
+    r.gamma = c->scene_gamma;
+    if (!p) {
+        if (ref_store) {  // evaluate at the store's sampling parameters
+            if (s.unknown >= 0 && !ref_store->ref_beta.empty()) {
+                CK(cudaMemcpyAsync(c->param_beta.p, ref_store->ref_beta.data(),
+                                   (size_t)c->V * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+                r.src[s.unknown] = c->param_beta.p;
+            }
+            r.kappa = ref_store->ref_kappa;
+            r.gamma = ref_store->ref_gamma;
+        }
+        return r;
+    }
+    if (p->beta && s.unknown >= 0) {
+        if ((long long)p->n_beta != c->V) throw Err(PRC_ERR_CONFIG, "params: beta size != voxel count");
+        CK(cudaMemcpyAsync(c->param_beta.p, p->beta, (size_t)c->V * sizeof(double),
+                           cudaMemcpyHostToDevice, c->stream));
+        r.src[s.unknown] = c->param_beta.p;
+    }
+    if (p->species_beta) {
+        for (int j = 0; j < s.n_species; ++j) {
+            if (!p->species_beta[j]) continue;
+            double* dst = c->species_t.p + (size_t)j * c->V;
+            CK(cudaMemcpyAsync(dst, p->species_beta[j], (size_t)c->V * sizeof(double),
+                               cudaMemcpyHostToDevice, c->stream));
+            r.src[j] = dst;
+        }
+    }
+    if (s.target >= 0) {
+        r.kappa = p->kappa_s;
+        r.gamma = p->gamma;
+    }
+    return r;
+}
+
+// ----------------------------------------------------------------------- K3 + K4 + K5
+struct EvalRun {
+    bool want_grad = false, per_species = false, legacy = false, normalize = true;
+    const double* weights = nullptr;  // device
+};
+
+// Runs K3 prep, K4 forward (+ image allreduce) and optionally K5 (+ grad allreduce).
+// Leaves raw sums in c->images / c->g_span / c->g_vert / c->g_phong; returns clamps.
+unsigned long long run_eval(prc_gpu_ctx* c, prc_gpu_store* st, const Resolved& r, const EvalRun& er,
+                            const double* phong_dev) {
+    const DScene& s = c->dsc;
+    cudaStream_t q = c->stream;
+    CK(cudaEventRecord(c->ev[0], q));
+    CK(launch_prep(s.n_species, c->V, r.src, st->br_tot64.p, c->sp_t.p, c->bt_tot.p, c->dbeta.p, q,
+                   &c->launches));
+    if (!phong_dev) {
+        const double ph[2] = {r.kappa, r.gamma};
+        CK(cudaMemcpyAsync(c->phong.p, ph, sizeof ph, cudaMemcpyHostToDevice, q));
+        phong_dev = c->phong.p;
+    }
+    const size_t slots = (size_t)s.n_det * (size_t)std::max<unsigned long long>(st->n_iv, 1);
+    st->ev_val.grow(slots);
+    st->ev_pix.grow(slots);
+    CK(cudaMemsetAsync(c->images.p, 0, c->images.bytes(), q));
+    CK(cudaMemsetAsync(c->clamps.p, 0, sizeof(unsigned long long), q));
+    EvalArgs ea{};
+    ea.sp_t = c->sp_t.p;
+    ea.sp_ref = st->sp_ref.p;
+    ea.bt_tot = c->bt_tot.p;
+    ea.br_tot = st->br_tot.p;
+    ea.dbeta = c->dbeta.p;
+    ea.phong = phong_dev;
+    ea.images = c->images.p;
+    ea.clamps = c->clamps.p;
+    ea.weights = er.weights;
+    ea.g_span = c->g_span.p;
+    ea.g_vert = c->g_vert.p;
+    ea.g_phong = c->g_phong.p;
+    ea.per_species = er.per_species ? 1 : 0;
+    ea.legacy = er.legacy ? 1 : 0;
+    ea.do_beta = s.has_medium && (s.unknown >= 0 || er.per_species) ? 1 : 0;
+    StoreView sv = st->view();
+    CK(cudaEventRecord(c->ev[1], q));
+    CK(launch_forward(s, sv, ea, q, &c->launches));
+    CK(cudaEventRecord(c->ev[2], q));
+    c->allreduce(c->images.p, (size_t)c->n_pix);
+    c->allreduce_u64(c->clamps.p, 1);
+    CK(cudaEventRecord(c->ev[3], q));
+    if (er.want_grad) {
+        CK(cudaMemsetAsync(c->g_span.p, 0, c->g_span.bytes(), q));
+        CK(cudaMemsetAsync(c->g_vert.p, 0, c->g_vert.bytes(), q));
+        CK(cudaMemsetAsync(c->g_phong.p, 0, 2 * sizeof(double), q));
+        CK(launch_gradient(s, sv, ea, q, &c->launches));
+    }
+    CK(cudaEventRecord(c->ev[4], q));
+    if (er.want_grad) {
+        c->allreduce(c->g_span.p, c->g_span.n);
+        c->allreduce(c->g_vert.p, c->g_vert.n);
+        c->allreduce(c->g_phong.p, 2);
+    }
+    unsigned long long cl = 0;
+    CK(cudaMemcpyAsync(&cl, c->clamps.p, sizeof cl, cudaMemcpyDeviceToHost, q));
+    return cl;
+}
+
+void record_timings(prc_gpu_ctx* c) {
+    c->sync();
+    float ms;
+    const int pairs[5][2] = {{0, 1}, {1, 2}, {2, 3}, {3, 4}, {4, 5}};
+    for (int i = 0; i < 5; ++i) {
+        CK(cudaEventElapsedTime(&ms, c->ev[pairs[i][0]], c->ev[pairs[i][1]]));
+        c->last_ms[i] = ms;
+    }
+    CK(cudaEventElapsedTime(&ms, c->ev[0], c->ev[5]));
+    c->last_ms[5] = ms;
+}
+
+// ----------------------------------------------------------------------- K1 trace
+// Builds a path-major store for this rank's shard, sampled under species values
+// `sp_dev` (n_species x V, fp64, device) and Phong values (kappa, gamma).
+std::unique_ptr<prc_gpu_store> trace_store(prc_gpu_ctx* c, const prc_gpu_render_opts* o,
+                                           const double* sp_dev, double kappa, double gamma,
+                                           const double* ref_beta_host_or_dev, bool ref_on_dev) {
+    const DScene& s = c->dsc;
+    cudaStream_t q = c->stream;
+    auto st = std::make_unique<prc_gpu_store>();
+    st->ctx = c;
+    const unsigned long long N = o->n_paths;
+    st->n_global = N;
+    st->stream_base = N * (unsigned long long)c->rank / (unsigned long long)c->world;
+    const unsigned long long end = N * (unsigned long long)(c->rank + 1) / (unsigned long long)c->world;
+    st->n = end - st->stream_base;
+    st->seed = o->seed;
+    st->ref_kappa = kappa;
+    st->ref_gamma = gamma;
+    const long long V = c->V;
+    // reference context of the store (make_context's ref side, pathstore.cpp:54-81)
+    st->br_tot64.alloc((size_t)std::max<long long>(V, 1));
+    st->sp_ref.alloc((size_t)std::max(1, s.n_species) * (size_t)std::max<long long>(V, 1));
+    st->br_tot.alloc((size_t)std::max<long long>(V, 1));
+    const double* src[PRC_MAX_SPECIES] = {};
+    for (int j = 0; j < s.n_species; ++j) src[j] = sp_dev + (size_t)j * V;
+    CK(launch_prep_ref(s.n_species, V, src, st->br_tot64.p, st->sp_ref.p, st->br_tot.p, nullptr, q,
+                       &c->launches));
+    if (s.unknown >= 0) {
+        st->ref_beta.resize((size_t)V);
+        CK(cudaMemcpyAsync(st->ref_beta.data(), ref_beta_host_or_dev ? ref_beta_host_or_dev
+                                                                      : sp_dev + (size_t)s.unknown * V,
+                           (size_t)V * sizeof(double),
+                           ref_on_dev || !ref_beta_host_or_dev ? cudaMemcpyDeviceToHost
+                                                               : cudaMemcpyHostToHost,
+                           q));
+    }
+    const unsigned long long n = st->n;
+    st->B.alloc(std::max<unsigned long long>(n, 1));
+    st->trunc.alloc(std::max<unsigned long long>(n, 1));
+    st->stream.alloc(std::max<unsigned long long>(n, 1));
+    // stream ids of a fresh shard are stream_base + i
+    {
+        std::vector<unsigned long long> ids(n);
+        for (unsigned long long i = 0; i < n; ++i) ids[i] = st->stream_base + i;
+        if (n)
+            CK(cudaMemcpyAsync(st->stream.p, ids.data(), n * sizeof(unsigned long long),
+                               cudaMemcpyHostToDevice, q));
+        c->sync();
+    }
+    TraceArgs a{};
+    a.beta_tot = st->br_tot64.p;
+    a.sp_beta = sp_dev;
+    a.seed = o->seed;
+    a.stream_base = st->stream_base;
+    a.n = n;
+    a.max_bounces = o->max_bounces > 0 ? o->max_bounces : 500;
+    a.max_events = o->max_scatter_events;
+    a.B = st->B.p;
+    a.trunc = st->trunc.p;
+    a.err = c->err.p;
+    CK(cudaMemsetAsync(c->err.p, 0, sizeof(int), q));
+    CK(launch_trace(s, a, false, q, &c->launches));
+    // offsets: exclusive scans of (B + 1) and (B - 1)+
+    c->u64tmp_a.grow(std::max<unsigned long long>(n, 1) * 2);
+    c->u64tmp_b.grow(std::max<unsigned long long>(n, 1) * 2);
+    unsigned long long* rt = c->u64tmp_a.p;
+    unsigned long long* it = c->u64tmp_a.p + std::max<unsigned long long>(n, 1);
+    st->rec_base.alloc(std::max<unsigned long long>(n, 1));
+    st->iv_base.alloc(std::max<unsigned long long>(n, 1));
+    st->stride.alloc(std::max<unsigned long long>(n, 1));
+    CK(launch_size_terms(st->B.p, (long long)n, rt, it, q, &c->launches));
+    CK(scan_u64(rt, c->u64tmp_b.p, (long long)n, &c->cub_tmp, &c->cub_bytes, q));
+    CK(scan_u64(it, c->u64tmp_b.p + std::max<unsigned long long>(n, 1), (long long)n, &c->cub_tmp,
+                &c->cub_bytes, q));
+    CK(launch_path_major_layout(c->u64tmp_b.p, c->u64tmp_b.p + std::max<unsigned long long>(n, 1),
+                                (long long)n, st->rec_base.p, st->stride.p, st->iv_base.p, q,
+                                &c->launches));
+    int errf = 0;
+    CK(cudaMemcpyAsync(&errf, c->err.p, sizeof errf, cudaMemcpyDeviceToHost, q));
+    unsigned long long last[4] = {0, 0, 0, 0};
+    uint32_t lastB = 0;
+    if (n) {
+        CK(cudaMemcpyAsync(&last[0], c->u64tmp_b.p + (n - 1), sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, q));
+        CK(cudaMemcpyAsync(&last[1], c->u64tmp_b.p + std::max<unsigned long long>(n, 1) + (n - 1),
+                           sizeof(unsigned long long), cudaMemcpyDeviceToHost, q));
+        CK(cudaMemcpyAsync(&lastB, st->B.p + (n - 1), sizeof lastB, cudaMemcpyDeviceToHost, q));
+    }
+    c->u32tmp.grow(1);
+    uint32_t maxB = 0;
+    if (n) {
+        CK(reduce_max_u32(st->B.p, (long long)n, c->u32tmp.p, &c->cub_tmp, &c->cub_bytes, q));
+        CK(cudaMemcpyAsync(&maxB, c->u32tmp.p, sizeof maxB, cudaMemcpyDeviceToHost, q));
+    }
+    c->sync();
+    if (errf) throw Err(PRC_ERR_CONFIG, "sample_direction: vacuum point");
+    st->max_B = (int)maxB;
+    st->n_rec = n ? last[0] + lastB + 1 : 0;
+    st->n_iv = n ? last[1] + (lastB >= 2 ? lastB - 1 : 0) : 0;
+    st->segments = st->n_rec - n;
+    st->alloc_records(std::max<unsigned long long>(st->n_rec, 1));
+    a.off = st->rec_base.p;
+    a.rec = st->rec_out();
+    CK(launch_trace(s, a, true, q, &c->launches));
+    // truncated count
+    {
+        std::vector<uint8_t> tr(n);
+        if (n) CK(cudaMemcpyAsync(tr.data(), st->trunc.p, n, cudaMemcpyDeviceToHost, q));
+        c->sync();
+        unsigned long long cnt = 0;
+        for (auto t : tr) cnt += t;
+        st->truncated = cnt;
+    }
+    return st;
+}
+
+// ----------------------------------------------------------------------- K2 sort
+void sort_store(prc_gpu_ctx* c, prc_gpu_store* st) {
+    if (st->n_global == 0 || (st->n == 0 && c->world == 1))
+        throw Err(PRC_ERR_CONFIG, "sort_by_size: empty store");
+    const long long n = (long long)st->n;
+    if (n == 0) {
+        st->sorted = true;
+        return;
+    }
+    cudaStream_t q = c->stream;
+    const int nb = st->max_B + 1;
+    const int tile = 4096;
+    const long long n_tiles = (n + tile - 1) / tile;
+    DBuf<unsigned long long> th, toff;
+    th.alloc((size_t)nb * n_tiles);
+    toff.alloc((size_t)nb * n_tiles);
+    CK(launch_sort_hist(st->B.p, n, nb, tile, th.p, q, &c->launches));
+    CK(scan_u64(th.p, toff.p, (long long)nb * n_tiles, &c->cub_tmp, &c->cub_bytes, q));
+    DBuf<uint32_t> perm;
+    perm.alloc((size_t)n);
+    CK(launch_sort_rank(st->B.p, n, nb, tile, toff.p, perm.p, q, &c->launches));
+    // bucket table: start of bin k = toff[k * n_tiles]
+    std::vector<unsigned long long> all((size_t)nb * n_tiles);
+    CK(cudaMemcpyAsync(all.data(), toff.p, all.size() * sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost, q));
+    c->sync();
+    std::vector<unsigned long long> bstart(nb + 1), brec(nb + 1), biv(nb + 1);
+    for (int k = 0; k < nb; ++k) bstart[k] = all[(size_t)k * n_tiles];
+    bstart[nb] = (unsigned long long)n;
+    unsigned long long R = 0, I = 0;
+    for (int k = 0; k <= nb; ++k) {
+        brec[k] = R;
+        biv[k] = I;
+        if (k < nb) {
+            const unsigned long long cnt = bstart[k + 1] - bstart[k];
+            R += cnt * (unsigned long long)(k + 1);
+            I += cnt * (unsigned long long)(k >= 2 ? k - 1 : 0);
+        }
+    }
+    DBuf<unsigned long long> d_bstart, d_brec, d_biv;
+    d_bstart.alloc(nb + 1);
+    d_brec.alloc(nb + 1);
+    d_biv.alloc(nb + 1);
+    CK(cudaMemcpyAsync(d_bstart.p, bstart.data(), (nb + 1) * 8, cudaMemcpyHostToDevice, q));
+    CK(cudaMemcpyAsync(d_brec.p, brec.data(), (nb + 1) * 8, cudaMemcpyHostToDevice, q));
+    CK(cudaMemcpyAsync(d_biv.p, biv.data(), (nb + 1) * 8, cudaMemcpyHostToDevice, q));
+    auto ns = std::make_unique<prc_gpu_store>();
+    ns->B.alloc((size_t)n);
+    ns->stream.alloc((size_t)n);
+    ns->trunc.alloc((size_t)n);
+    ns->rec_base.alloc((size_t)n);
+    ns->stride.alloc((size_t)n);
+    ns->iv_base.alloc((size_t)n);
+    CK(launch_bucket_layout(perm.p, st->B.p, st->stream.p, st->trunc.p, n, d_bstart.p, d_brec.p,
+                            d_biv.p, ns->B.p, ns->stream.p, ns->trunc.p, ns->rec_base.p,
+                            ns->stride.p, ns->iv_base.p, q, &c->launches));
+    ns->alloc_records(st->n_rec);
+    CK(launch_gather_records(st->view(), perm.p, n, ns->rec_base.p, ns->stride.p, ns->rec_out(), q,
+                             &c->launches));
+    c->sync();
+    st->B.swap(ns->B);
+    st->stream.swap(ns->stream);
+    st->trunc.swap(ns->trunc);
+    st->rec_base.swap(ns->rec_base);
+    st->stride.swap(ns->stride);
+    st->iv_base.swap(ns->iv_base);
+    st->px.swap(ns->px);
+    st->py.swap(ns->py);
+    st->pz.swap(ns->pz);
+    st->dx.swap(ns->dx);
+    st->dy.swap(ns->dy);
+    st->dz.swap(ns->dz);
+    st->tt.swap(ns->tt);
+    st->ct.swap(ns->ct);
+    st->vox.swap(ns->vox);
+    st->meta.swap(ns->meta);
+    st->sorted = true;
+}
+
+// ----------------------------------------------------------------------- PSTR I/O
+template <class T>
+void put(std::ofstream& os, const T& v) {
+    os.write(reinterpret_cast<const char*>(&v), sizeof(T));
+}
+template <class T>
+T get(std::ifstream& is) {
+    T v{};
+    is.read(reinterpret_cast<char*>(&v), sizeof(T));
+    return v;
+}
+
+template <class T>
+std::vector<T> d2h(const DBuf<T>& b, size_t n, cudaStream_t q) {
+    std::vector<T> h(n);
+    if (n) CK(cudaMemcpyAsync(h.data(), b.p, n * sizeof(T), cudaMemcpyDeviceToHost, q));
+    return h;
+}
+
+void export_pstr(prc_gpu_ctx* c, prc_gpu_store* st, const std::string& path) {
+    const DScene& s = c->dsc;
+    cudaStream_t q = c->stream;
+    const unsigned long long n = st->n;
+    auto B = d2h(st->B, n, q);
+    auto streams = d2h(st->stream, n, q);
+    auto trunc = d2h(st->trunc, n, q);
+    auto rb = d2h(st->rec_base, n, q);
+    auto rs = d2h(st->stride, n, q);
+    auto ib = d2h(st->iv_base, n, q);
+    auto px = d2h(st->px, st->n_rec, q), py = d2h(st->py, st->n_rec, q), pz = d2h(st->pz, st->n_rec, q);
+    auto dx = d2h(st->dx, st->n_rec, q), dy = d2h(st->dy, st->n_rec, q), dz = d2h(st->dz, st->n_rec, q);
+    auto tt = d2h(st->tt, st->n_rec, q), ct = d2h(st->ct, st->n_rec, q);
+    auto vox = d2h(st->vox, st->n_rec, q);
+    auto meta = d2h(st->meta, st->n_rec, q);
+    // events on the device
+    const size_t slots = (size_t)s.n_det * (size_t)std::max<unsigned long long>(st->n_iv, 1);
+    DBuf<int32_t> epix;
+    DBuf<double> ecos, egeom, eray;
+    epix.alloc(slots);
+    ecos.alloc(slots);
+    egeom.alloc(slots);
+    eray.alloc(4 * slots);
+    CK(launch_events(s, st->view(), epix.p, ecos.p, egeom.p, eray.p, q, &c->launches));
+    auto hpix = d2h(epix, slots, q);
+    auto hcos = d2h(ecos, slots, q);
+    auto hgeom = d2h(egeom, slots, q);
+    auto hray = d2h(eray, 4 * slots, q);
+    c->sync();
+    // rays: every segment b = 1..B and every event's LE connection
+    std::vector<double> rays;
+    auto rec = [&](unsigned long long p, int b) { return rb[p] + (unsigned long long)b * rs[p]; };
+    for (unsigned long long p = 0; p < n; ++p) {
+        for (int b = 1; b <= (int)B[p]; ++b) {
+            const auto r0 = rec(p, b - 1), r1 = rec(p, b);
+            rays.insert(rays.end(), {px[r0], py[r0], pz[r0], dx[r1], dy[r1], dz[r1], tt[r1]});
+        }
+        for (int b = 1; b < (int)B[p]; ++b) {
+            const auto r1 = rec(p, b);
+            const unsigned long long iv = ib[p] + (unsigned long long)(b - 1) * rs[p];
+            for (int k = 0; k < s.n_det; ++k) {
+                const size_t slot = (size_t)k * st->n_iv + iv;
+                if (hpix[slot] < 0) continue;
+                rays.insert(rays.end(), {px[r1], py[r1], pz[r1], hray[4 * slot], hray[4 * slot + 1],
+                                         hray[4 * slot + 2], hray[4 * slot + 3]});
+            }
+        }
+    }
+    const long long nr = (long long)(rays.size() / 7);
+    std::vector<uint32_t> counts(nr), svox;
+    std::vector<double> slen;
+    std::vector<unsigned long long> offs(nr + 1, 0);
+    if (s.has_medium && nr > 0) {
+        DBuf<double> drays;
+        DBuf<uint32_t> dcounts, dvox;
+        DBuf<unsigned long long> doff;
+        DBuf<double> dlen;
+        drays.alloc(rays.size());
+        dcounts.alloc(nr);
+        CK(cudaMemcpyAsync(drays.p, rays.data(), rays.size() * 8, cudaMemcpyHostToDevice, q));
+        CK(launch_walk(s, drays.p, nr, dcounts.p, nullptr, nullptr, nullptr, q, &c->launches));
+        counts = d2h(dcounts, nr, q);
+        c->sync();
+        for (long long i = 0; i < nr; ++i) offs[i + 1] = offs[i] + counts[i];
+        const unsigned long long tot = offs[nr];
+        doff.alloc(nr);
+        dvox.alloc(std::max<unsigned long long>(tot, 1));
+        dlen.alloc(std::max<unsigned long long>(tot, 1));
+        CK(cudaMemcpyAsync(doff.p, offs.data(), nr * 8, cudaMemcpyHostToDevice, q));
+        CK(launch_walk(s, drays.p, nr, dcounts.p, doff.p, dvox.p, dlen.p, q, &c->launches));
+        svox = d2h(dvox, tot, q);
+        slen = d2h(dlen, tot, q);
+        c->sync();
+    }
+    std::ofstream os(path, std::ios::binary);
+    if (!os) throw Err(PRC_ERR_IO, "save_store: cannot open " + path);
+    os.write("PSTR", 4);
+    put<uint32_t>(os, 1u);
+    put<uint64_t>(os, n);
+    put<uint64_t>(os, st->generation);
+    put<uint64_t>(os, st->seed);
+    put<uint8_t>(os, st->sorted ? 1 : 0);
+    put<uint64_t>(os, st->ref_beta.size());
+    for (double b : st->ref_beta) put<double>(os, b);
+    put<double>(os, st->ref_kappa);
+    put<double>(os, st->ref_gamma);
+    long long ray = 0;
+    for (unsigned long long p = 0; p < n; ++p) {
+        const int Bp = (int)B[p];
+        put<uint64_t>(os, streams[p]);
+        put<uint8_t>(os, trunc[p]);
+        const auto r0 = rec(p, 0);
+        put<double>(os, dx[r0]);
+        put<double>(os, dy[r0]);
+        put<double>(os, dz[r0]);
+        put<uint32_t>(os, (uint32_t)(Bp + 1));
+        uint32_t span_pos = 0;
+        const long long seg_ray0 = ray;
+        for (int b = 0; b <= Bp; ++b) {
+            const auto r = rec(p, b);
+            const uint32_t m = meta[r];
+            const uint32_t kind = m & 0xffu;
+            double cos_in = 1.0, cos_out = 1.0;
+            if (kind == VK_SURFACE) {  // facing normal; cos_out from the continuation direction
+                const prc_surface_desc& sf = c->surfaces[(int)(int16_t)(m >> 16)];
+                H3 x{px[r], py[r], pz[r]}, din{dx[r], dy[r], dz[r]}, nn;
+                if (sf.kind == PRC_SURF_SPHERE)
+                    nn = hnormalized(hsub(x, h3(sf.center)));
+                else
+                    nn = {sf.axis == 0 ? sf.normal_sign : 0.0, sf.axis == 1 ? sf.normal_sign : 0.0,
+                          sf.axis == 2 ? sf.normal_sign : 0.0};
+                if (hdot(nn, din) > 0.0) nn = {-nn.x, -nn.y, -nn.z};
+                cos_in = -hdot(nn, din);
+                if (b < Bp) {
+                    const auto rn = rec(p, b + 1);
+                    cos_out = hdot(nn, H3{dx[rn], dy[rn], dz[rn]});
+                }
+            }
+            uint32_t sb = 0, se = 0;
+            if (b >= 1) {
+                sb = span_pos;
+                span_pos += s.has_medium ? counts[seg_ray0 + (b - 1)] : 0;
+                se = span_pos;
+            }
+            put<double>(os, px[r]);
+            put<double>(os, py[r]);
+            put<double>(os, pz[r]);
+            put<double>(os, ct[r]);
+            put<double>(os, cos_in);
+            put<double>(os, cos_out);
+            put<uint32_t>(os, sb);
+            put<uint32_t>(os, se);
+            put<int32_t>(os, vox[r]);
+            put<int16_t>(os, (int16_t)(m >> 16));
+            put<int8_t>(os, (int8_t)((m >> 8) & 0xffu));
+            put<uint8_t>(os, (uint8_t)kind);
+        }
+        put<uint32_t>(os, span_pos);
+        for (int b = 1; b <= Bp; ++b) {
+            const long long rr = seg_ray0 + (b - 1);
+            if (!s.has_medium) continue;
+            for (unsigned long long k = offs[rr]; k < offs[rr + 1]; ++k) {
+                put<uint32_t>(os, svox[k]);
+                put<double>(os, slen[k]);
+            }
+        }
+        ray += Bp;
+        // events
+        uint32_t ne = 0;
+        for (int b = 1; b < Bp; ++b) {
+            const unsigned long long iv = ib[p] + (unsigned long long)(b - 1) * rs[p];
+            for (int k = 0; k < s.n_det; ++k) ne += hpix[(size_t)k * st->n_iv + iv] >= 0 ? 1 : 0;
+        }
+        put<uint32_t>(os, ne);
+        const long long le_ray0 = ray;
+        uint32_t le_pos = 0;
+        long long er = le_ray0;
+        for (int b = 1; b < Bp; ++b) {
+            const unsigned long long iv = ib[p] + (unsigned long long)(b - 1) * rs[p];
+            for (int k = 0; k < s.n_det; ++k) {
+                const size_t slot = (size_t)k * st->n_iv + iv;
+                if (hpix[slot] < 0) continue;
+                const uint32_t cnt = s.has_medium ? counts[er] : 0;
+                put<uint32_t>(os, (uint32_t)b);
+                put<uint16_t>(os, (uint16_t)k);
+                put<int32_t>(os, hpix[slot]);
+                put<double>(os, hcos[slot]);
+                put<double>(os, hgeom[slot]);
+                put<uint32_t>(os, le_pos);
+                put<uint32_t>(os, le_pos + cnt);
+                le_pos += cnt;
+                ++er;
+            }
+        }
+        put<uint32_t>(os, le_pos);
+        for (long long rr = le_ray0; rr < er; ++rr) {
+            if (!s.has_medium) continue;
+            for (unsigned long long k = offs[rr]; k < offs[rr + 1]; ++k) {
+                put<uint32_t>(os, svox[k]);
+                put<double>(os, slen[k]);
+            }
+        }
+        ray = er;
+    }
+    if (!os) throw Err(PRC_ERR_IO, "save_store: write failure on " + path);
+}
+
+std::unique_ptr<prc_gpu_store> import_pstr(prc_gpu_ctx* c, const std::string& path) {
+    const DScene& s = c->dsc;
+    std::ifstream is(path, std::ios::binary);
+    if (!is) throw Err(PRC_ERR_IO, "load_store: cannot open " + path);
+    char magic[4];
+    is.read(magic, 4);
+    if (!is || std::memcmp(magic, "PSTR", 4) != 0)
+        throw Err(PRC_ERR_IO, "load_store: bad magic at offset 0 in " + path);
+    if (get<uint32_t>(is) != 1) throw Err(PRC_ERR_IO, "load_store: unsupported version");
+    auto st = std::make_unique<prc_gpu_store>();
+    st->ctx = c;
+    const uint64_t count = get<uint64_t>(is);
+    st->generation = get<uint64_t>(is);
+    st->seed = get<uint64_t>(is);
+    st->sorted = get<uint8_t>(is) != 0;
+    const uint64_t nb = get<uint64_t>(is);
+    st->ref_beta.resize(nb);
+    for (auto& b : st->ref_beta) b = get<double>(is);
+    st->ref_kappa = get<double>(is);
+    st->ref_gamma = get<double>(is);
+    if (!is) throw Err(PRC_ERR_IO, "load_store: truncated file " + path);
+    if (s.unknown >= 0 && !st->ref_beta.empty() && (long long)nb != c->V)
+        throw Err(PRC_ERR_CONFIG, "load_store: reference beta size != voxel count");
+    // this rank's slice of the records
+    const uint64_t lo = count * (uint64_t)c->rank / (uint64_t)c->world;
+    const uint64_t hi = count * (uint64_t)(c->rank + 1) / (uint64_t)c->world;
+    st->n_global = count;
+    st->stream_base = lo;
+    st->n = hi - lo;
+    std::vector<uint32_t> B;
+    std::vector<unsigned long long> streams, rb, ib;
+    std::vector<uint8_t> trunc;
+    std::vector<double> px, py, pz, dx, dy, dz, tt, ct;
+    std::vector<int32_t> vox;
+    std::vector<uint32_t> meta;
+    unsigned long long n_iv = 0;
+    int maxB = 0;
+    for (uint64_t i = 0; i < count; ++i) {
+        const uint64_t stream = get<uint64_t>(is);
+        const uint8_t tr = get<uint8_t>(is);
+        H3 d0{get<double>(is), get<double>(is), get<double>(is)};
+        const uint32_t nv = get<uint32_t>(is);
+        if (!is || nv == 0) throw Err(PRC_ERR_IO, "load_store: truncated file " + path);
+        const bool mine = i >= lo && i < hi;
+        H3 prev{0, 0, 0}, pdir = d0;
+        if (mine) {
+            B.push_back(nv - 1);
+            streams.push_back(stream);
+            trunc.push_back(tr);
+            rb.push_back(px.size());
+            ib.push_back(n_iv);
+            n_iv += nv >= 3 ? nv - 2 : 0;
+            maxB = std::max(maxB, (int)nv - 1);
+        }
+        for (uint32_t k = 0; k < nv; ++k) {
+            H3 x{get<double>(is), get<double>(is), get<double>(is)};
+            const double cth = get<double>(is);
+            (void)get<double>(is);  // cos_in (not on the recycling path)
+            (void)get<double>(is);  // cos_out
+            (void)get<uint32_t>(is);
+            (void)get<uint32_t>(is);
+            const int32_t vx = get<int32_t>(is);
+            const int16_t sf = get<int16_t>(is);
+            const int8_t spc = get<int8_t>(is);
+            const uint8_t kind = get<uint8_t>(is);
+            if (!mine) continue;
+            // incoming direction: dir0 for the first segment, the chord direction after
+            H3 d = d0;
+            double t = 0.0;
+            if (k >= 1) {
+                const H3 ch = hsub(x, prev);
+                t = hnorm(ch);
+                d = k == 1 ? d0 : (t > 0.0 ? hnormalized(ch) : pdir);
+            }
+            px.push_back(x.x);
+            py.push_back(x.y);
+            pz.push_back(x.z);
+            dx.push_back(d.x);
+            dy.push_back(d.y);
+            dz.push_back(d.z);
+            tt.push_back(t);
+            ct.push_back(cth);
+            vox.push_back(vx);
+            meta.push_back((uint32_t)(kind & 0xffu) | ((uint32_t)(uint8_t)spc << 8) |
+                           ((uint32_t)(uint16_t)sf << 16));
+            prev = x;
+            pdir = d;
+        }
+        // spans, events and LE spans are recomputed on the device: skip them
+        uint32_t ns = get<uint32_t>(is);
+        is.seekg((std::streamoff)ns * 12, std::ios::cur);
+        uint32_t ne = get<uint32_t>(is);
+        is.seekg((std::streamoff)ne * 34, std::ios::cur);
+        uint32_t nl = get<uint32_t>(is);
+        is.seekg((std::streamoff)nl * 12, std::ios::cur);
+        if (!is) throw Err(PRC_ERR_IO, "load_store: truncated file " + path);
+    }
+    cudaStream_t q = c->stream;
+    const unsigned long long n = st->n;
+    st->max_B = maxB;
+    st->n_iv = n_iv;
+    st->n_rec = px.size();
+    st->segments = st->n_rec - n;
+    for (auto t : trunc) st->truncated += t;
+    auto up = [&](auto& dst, const auto& src) {
+        using T = typename std::decay_t<decltype(src)>::value_type;
+        dst.alloc(std::max<size_t>(src.size(), 1));
+        if (!src.empty())
+            CK(cudaMemcpyAsync(dst.p, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice, q));
+    };
+    std::vector<uint32_t> stride(n, 1u);
+    up(st->B, B);
+    up(st->stream, streams);
+    up(st->trunc, trunc);
+    up(st->rec_base, rb);
+    up(st->iv_base, ib);
+    up(st->stride, stride);
+    up(st->px, px);
+    up(st->py, py);
+    up(st->pz, pz);
+    up(st->dx, dx);
+    up(st->dy, dy);
+    up(st->dz, dz);
+    up(st->tt, tt);
+    up(st->ct, ct);
+    up(st->vox, vox);
+    up(st->meta, meta);
+    // reference-side context from the stored ref params
+    const long long V = c->V;
+    st->br_tot64.alloc((size_t)std::max<long long>(V, 1));
+    st->sp_ref.alloc((size_t)std::max(1, s.n_species) * (size_t)std::max<long long>(V, 1));
+    st->br_tot.alloc((size_t)std::max<long long>(V, 1));
+    const double* src[PRC_MAX_SPECIES] = {};
+    for (int j = 0; j < s.n_species; ++j) src[j] = c->scene_sp.p + (size_t)j * V;
+    if (s.unknown >= 0 && !st->ref_beta.empty()) {
+        c->trace_sp.grow((size_t)V);
+        CK(cudaMemcpyAsync(c->trace_sp.p, st->ref_beta.data(), (size_t)V * 8, cudaMemcpyHostToDevice, q));
+        src[s.unknown] = c->trace_sp.p;
+    }
+    CK(launch_prep_ref(s.n_species, V, src, st->br_tot64.p, st->sp_ref.p, st->br_tot.p, nullptr, q,
+                       &c->launches));
+    c->sync();
+    return st;
+}
+
+void copy_out(prc_gpu_ctx* c, double* host, const double* dev, size_t n) {
+    if (host && n) CK(cudaMemcpyAsync(host, dev, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+}
+
+}  // namespace
+
+// =============================================================================== C ABI
+PRC_EXPORT const char* prc_gpu_version(void) { return "pathrec-b200 0.1 (sm_100a)"; }
+PRC_EXPORT const char* prc_gpu_last_error(void) { return g_last_error.c_str(); }
+
+static int ctx_init(prc_gpu_ctx* c, int device) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0)
+        throw Err(PRC_ERR_CUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+    if (device < 0 || device >= n) throw Err(PRC_ERR_INVALID, "device index out of range");
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) throw Err(PRC_ERR_CUDA, "pathrec-b200 requires an sm_100 (B200) device");
+    c->device = device;
+    CK(cudaSetDevice(device));
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    for (auto& ev : c->ev) CK(cudaEventCreate(&ev));
+    return PRC_OK;
+}
+
+PRC_EXPORT int prc_gpu_ctx_create(int device, prc_gpu_ctx** out) {
+    if (!out) return fail(PRC_ERR_INVALID, "prc_gpu_ctx_create: null argument");
+    ABI_TRY
+    auto c = std::make_unique<prc_gpu_ctx>();
+    ctx_init(c.get(), device);
+    *out = c.release();
+    ABI_CATCH
+}
+
+PRC_EXPORT int prc_gpu_nccl_unique_id(void* out128) {
+    if (!out128) return fail(PRC_ERR_INVALID, "prc_gpu_nccl_unique_id: null argument");
+    ABI_TRY
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    ncclUniqueId id;
+    NK(ncclGetUniqueId(&id));
+    std::memcpy(out128, &id, sizeof id);
+    ABI_CATCH
+}
+
+PRC_EXPORT int prc_gpu_ctx_create_rank(int device, int rank, int world, const void* nccl_id,
+                                       prc_gpu_ctx** out) {
+    if (!out || (world > 1 && !nccl_id)) return fail(PRC_ERR_INVALID, "prc_gpu_ctx_create_rank: null argument");
+    if (world < 1 || rank < 0 || rank >= world) return fail(PRC_ERR_INVALID, "rank/world out of range");
+    ABI_TRY
+    auto c = std::make_unique<prc_gpu_ctx>();
+    ctx_init(c.get(), device);
+    c->rank = rank;
+    c->world = world;
+    if (world > 1) {
+        ncclUniqueId id;
+        std::memcpy(&id, nccl_id, sizeof id);
+        NK(ncclCommInitRank(&c->comm, world, id, rank));
+    }
+    *out = c.release();
+    ABI_CATCH
+}
+
+PRC_EXPORT void prc_gpu_ctx_destroy(prc_gpu_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    delete ctx;
+}
+
+PRC_EXPORT int prc_gpu_ctx_rank(const prc_gpu_ctx* ctx, int* rank, int* world) {
+    if (!ctx || !rank || !world) return fail(PRC_ERR_INVALID, "prc_gpu_ctx_rank: null argument");
+    *rank = ctx->rank;
+    *world = ctx->world;
+    return PRC_OK;
+}
+
+PRC_EXPORT int prc_gpu_scene_upload(prc_gpu_ctx* ctx, const prc_scene_desc* scene) {
+    if (!ctx || !scene) return fail(PRC_ERR_INVALID, "prc_gpu_scene_upload: null argument");
+    ABI_TRY
+    begin(ctx);
+    upload_scene(ctx, scene);
+    ABI_CATCH
+}
+
+PRC_EXPORT int prc_gpu_scene_voxel_count(const prc_gpu_ctx* ctx, uint64_t* out) {
+    if (!ctx || !out) return fail(PRC_ERR_INVALID, "null argument");
+    *out = (uint64_t)ctx->V;
+    return PRC_OK;
+}
+
+PRC_EXPORT int prc_gpu_scene_pixel_count(const prc_gpu_ctx* ctx, uint64_t* out) {
+    if (!ctx || !out) return fail(PRC_ERR_INVALID, "null argument");
+    *out = (uint64_t)ctx->n_pix;
+    return PRC_OK;
+}
+
+PRC_EXPORT int prc_gpu_render(prc_gpu_ctx* ctx, const prc_gpu_render_opts* opts,
+                              const prc_gpu_params* params, double* images_out,
+                              uint64_t* truncated_out, prc_gpu_store** store_out) {
+    if (!ctx || !opts) return fail(PRC_ERR_INVALID, "prc_gpu_render: null argument");
+    if (opts->n_paths == 0) return fail(PRC_ERR_CONFIG, "prc_gpu_render: n_paths must be >= 1");
+    ABI_TRY
+    begin(ctx);
+    ctx->check_scene();
+    const DScene& s = ctx->dsc;
+    // bind_params: sampling species values (inverse.cpp:144-150)
+    Resolved r = resolve_params(ctx, params, nullptr);
+    const double* beta_u = (s.unknown >= 0 && params && params->beta) ? ctx->param_beta.p : nullptr;
+    CK(launch_set_species(s.n_species, ctx->V, s.unknown, ctx->scene_sp.p, beta_u, ctx->trace_sp.p,
+                          ctx->stream, &ctx->launches));
+    if (params && params->species_beta)
+        for (int j = 0; j < s.n_species; ++j)
+            if (params->species_beta[j])
+                CK(cudaMemcpyAsync(ctx->trace_sp.p + (size_t)j * ctx->V, r.src[j],
+                                   (size_t)ctx->V * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+    auto st = trace_store(ctx, opts, ctx->trace_sp.p, r.kappa, r.gamma, nullptr, true);
+    // fresh evaluation at the sampling point (render's evaluate_store, transport.cpp:432-435)
+    Resolved rr;
+    for (int j = 0; j < s.n_species; ++j) rr.src[j] = ctx->trace_sp.p + (size_t)j * ctx->V;
+    rr.kappa = r.kappa;
+    rr.gamma = r.gamma;
+    EvalRun er;
+    run_eval(ctx, st.get(), rr, er, nullptr);
+    CK(launch_scale(ctx->images.p, ctx->n_pix, 1.0 / (double)opts->n_paths, ctx->stream, &ctx->launches));
+    copy_out(ctx, images_out, ctx->images.p, (size_t)ctx->n_pix);
+    ctx->sync();
+    if (truncated_out) {
+        double t = (double)st->truncated;
+        if (ctx->world > 1) {
+            CK(cudaMemcpy(ctx->loss.p, &t, 8, cudaMemcpyHostToDevice));
+            ctx->allreduce(ctx->loss.p, 1);
+            ctx->sync();
+            CK(cudaMemcpy(&t, ctx->loss.p, 8, cudaMemcpyDeviceToHost));
+        }
+        *truncated_out = (uint64_t)t;
+    }
+    if (store_out) *store_out = st.release();
+    ABI_CATCH
+}
+
+PRC_EXPORT int prc_gpu_sort_by_size(prc_gpu_ctx* ctx, prc_gpu_store* store) {
+    if (!ctx || !store) return fail(PRC_ERR_INVALID, "prc_gpu_sort_by_size: null argument");
+    ABI_TRY
+    begin(ctx);
+    sort_store(ctx, store);
+    ABI_CATCH
+}
+
+PRC_EXPORT int prc_gpu_store_info_get(const prc_gpu_store* st, prc_gpu_store_info* o) {
+    if (!st || !o) return fail(PRC_ERR_INVALID, "prc_gpu_store_info_get: null argument");
+    o->n_paths = st->n;
+    o->n_paths_global = st->n_global;
+    o->stream_base = st->stream_base;
+    o->segments = st->segments;
+    o->vertices = st->n_rec;
+    o->interaction_vertices = st->n_iv;
+    o->truncated = st->truncated;
+    o->seed = st->seed;
+    o->generation = st->generation;
+    o->sorted = st->sorted ? 1 : 0;
+    o->max_size = st->max_B;
+    o->device_bytes = st->device_bytes();
+    return PRC_OK;
+}
+
+PRC_EXPORT int prc_gpu_store_streams(const prc_gpu_store* st, uint64_t* out) {
+    if (!st || !out) return fail(PRC_ERR_INVALID, "prc_gpu_store_streams: null argument");
+    ABI_TRY
+    begin(st->ctx);
+    if (st->n) CK(cudaMemcpy(out, st->stream.p, st->n * 8, cudaMemcpyDeviceToHost));
+    ABI_CATCH
+}
+
+PRC_EXPORT int prc_gpu_store_sizes(const prc_gpu_store* st, uint32_t* out) {
+    if (!st || !out) return fail(PRC_ERR_INVALID, "prc_gpu_store_sizes: null argument");
+    ABI_TRY
+    begin(st->ctx);
+    if (st->n) CK(cudaMemcpy(out, st->B.p, st->n * 4, cudaMemcpyDeviceToHost));
+    ABI_CATCH
+}
+
+PRC_EXPORT int prc_gpu_store_export_pstr(prc_gpu_ctx* ctx, const prc_gpu_store* store,
+                                         const char* path) {
+    if (!ctx || !store || !path) return fail(PRC_ERR_INVALID, "prc_gpu_store_export_pstr: null argument");
+    ABI_TRY
+    begin(ctx);
+    export_pstr(ctx, const_cast<prc_gpu_store*>(store), path);
+    ABI_CATCH
+}
+
+PRC_EXPORT int prc_gpu_store_import_pstr(prc_gpu_ctx* ctx, const char* path, prc_gpu_store** out) {
+    if (!ctx || !path || !out) return fail(PRC_ERR_INVALID, "prc_gpu_store_import_pstr: null argument");
+    ABI_TRY
+    begin(ctx);
+    ctx->check_scene();
+    *out = import_pstr(ctx, path).release();
+    ABI_CATCH
+}
+
+PRC_EXPORT int prc_gpu_store_set_generation(prc_gpu_store* st, uint64_t g) {
+    if (!st) return fail(PRC_ERR_INVALID, "null store");
+    st->generation = g;
+    return PRC_OK;
+}
+
+PRC_EXPORT void prc_gpu_store_free(prc_gpu_store* st) {
+    if (!st) return;
+    cudaSetDevice(st->ctx->device);
+    delete st;
+}
+
+PRC_EXPORT int prc_gpu_evaluate(prc_gpu_ctx* ctx, const prc_gpu_store* store,
+                                const prc_gpu_params* params, const prc_gpu_eval_opts* opts,
+                                prc_gpu_eval_result* res) {
+    if (!ctx || !store || !res) return fail(PRC_ERR_INVALID, "prc_gpu_evaluate: null argument");
+    const int flags = opts ? opts->flags : PRC_EVAL_NORMALIZE;
+    if (flags & PRC_EVAL_SELF_NORMALIZE)
+        return fail(PRC_ERR_CONFIG, "self_normalize is not supported by the recycling engine");
+    ABI_TRY
+    begin(ctx);
+    ctx->check_scene();
+    auto* st = const_cast<prc_gpu_store*>(store);
+    Resolved r = resolve_params(ctx, params, st);
+    EvalRun er;
+    er.want_grad = (flags & PRC_EVAL_WANT_GRAD) != 0;
+    er.per_species = (flags & PRC_EVAL_PER_SPECIES) != 0;
+    er.legacy = (flags & PRC_EVAL_LEGACY_SCORE) != 0;
+    if (er.want_grad && opts && opts->pixel_weights) {
+        CK(cudaMemcpyAsync(ctx->weights.p, opts->pixel_weights, (size_t)ctx->n_pix * 8,
+                           cudaMemcpyHostToDevice, ctx->stream));
+        er.weights = ctx->weights.p;
+    }
+    const unsigned long long cl = run_eval(ctx, st, r, er, nullptr);
+    const double scale = (flags & PRC_EVAL_NORMALIZE) && st->n_global ? 1.0 / (double)st->n_global : 1.0;
+    CK(launch_scale(ctx->images.p, ctx->n_pix, scale, ctx->stream, &ctx->launches));
+    copy_out(ctx, res->images, ctx->images.p, (size_t)ctx->n_pix);
+    const DScene& s = ctx->dsc;
+    res->grad_kappa = res->grad_gamma = 0.0;
+    if (er.want_grad) {
+        const int n_out = er.per_species ? s.n_species : 1;
+        if (s.has_medium && (s.unknown >= 0 || er.per_species)) {
+            CK(launch_combine_grad(ctx->g_span.p, ctx->g_vert.p, n_out, ctx->V, scale, ctx->g_out.p,
+                                   ctx->stream, &ctx->launches));
+            copy_out(ctx, res->grad_beta, ctx->g_out.p, (size_t)n_out * ctx->V);
+        }
+        double gp[2] = {0, 0};
+        CK(cudaMemcpyAsync(gp, ctx->g_phong.p, sizeof gp, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaEventRecord(ctx->ev[5], ctx->stream));
+        record_timings(ctx);
+        res->grad_kappa = gp[0] * scale;
+        res->grad_gamma = gp[1] * scale;
+    } else {
+        CK(cudaEventRecord(ctx->ev[5], ctx->stream));
+        record_timings(ctx);
+    }
+    res->clamp_events = cl;
+    res->mean_correction = 1.0;
+    ABI_CATCH
+}
+
+// ------------------------------------------------------------------ Algorithm 2 (device)
+static void opt_init(prc_gpu_ctx* c, const prc_gpu_params* initial, const double* gt,
+                     const prc_gpu_adam_config* adam) {
+    const DScene& s = c->dsc;
+    cudaStream_t q = c->stream;
+    if (s.unknown >= 0) {
+        c->opt_mode = 0;
+        c->opt_n = c->V;
+        c->opt_x.alloc((size_t)c->V);
+        if (initial && initial->beta) {
+            if ((long long)initial->n_beta != c->V) throw Err(PRC_ERR_CONFIG, "initial beta size != voxel count");
+            CK(cudaMemcpyAsync(c->opt_x.p, initial->beta, (size_t)c->V * 8, cudaMemcpyHostToDevice, q));
+        } else {
+            CK(cudaMemcpyAsync(c->opt_x.p, c->scene_sp.p + (size_t)s.unknown * c->V, (size_t)c->V * 8,
+                               cudaMemcpyDeviceToDevice, q));
+        }
+    } else if (s.target >= 0) {
+        c->opt_mode = 1;
+        c->opt_n = 2;
+        c->opt_x.alloc(2);
+        const double kg[2] = {initial ? initial->kappa_s : c->scene_kappa,
+                              initial ? initial->gamma : c->scene_gamma};
+        CK(cudaMemcpyAsync(c->opt_x.p, kg, sizeof kg, cudaMemcpyHostToDevice, q));
+    } else {
+        throw Err(PRC_ERR_CONFIG, "scene declares no unknown species or target surface");
+    }
+    c->opt_m1.alloc((size_t)c->opt_n);
+    c->opt_m2.alloc((size_t)c->opt_n);
+    CK(cudaMemsetAsync(c->opt_m1.p, 0, c->opt_m1.bytes(), q));
+    CK(cudaMemsetAsync(c->opt_m2.p, 0, c->opt_m2.bytes(), q));
+    c->opt_gt.alloc((size_t)c->n_pix);
+    CK(cudaMemcpyAsync(c->opt_gt.p, gt, (size_t)c->n_pix * 8, cudaMemcpyHostToDevice, q));
+    c->adam = adam ? *adam : prc_gpu_adam_config{1e7, 0.9, 0.999, 1e-8, 1, nullptr, 0};
+    c->n_step_scale = adam && adam->step_scale ? adam->n_step_scale : 0;
+    c->opt_step_scale.alloc((size_t)std::max(1, c->n_step_scale));
+    if (c->n_step_scale)
+        CK(cudaMemcpyAsync(c->opt_step_scale.p, adam->step_scale, (size_t)c->n_step_scale * 8,
+                           cudaMemcpyHostToDevice, q));
+    c->opt_t = 0;
+    c->sync();
+    c->opt_ready = true;
+}
+
+// Current sampling species values (device fp64) for a resample under the iterate.
+static void bind_trace_species(prc_gpu_ctx* c) {
+    const DScene& s = c->dsc;
+    CK(launch_set_species(s.n_species, c->V, s.unknown, c->scene_sp.p,
+                          c->opt_mode == 0 ? c->opt_x.p : nullptr, c->trace_sp.p, c->stream,
+                          &c->launches));
+}
+
+static double opt_step(prc_gpu_ctx* c, prc_gpu_store* st) {
+    const DScene& s = c->dsc;
+    cudaStream_t q = c->stream;
+    Resolved r;
+    for (int j = 0; j < s.n_species; ++j) r.src[j] = c->scene_sp.p + (size_t)j * c->V;
+    const double* phong_dev = nullptr;
+    if (c->opt_mode == 0) {
+        r.src[s.unknown] = c->opt_x.p;
+        r.kappa = c->scene_kappa;
+        r.gamma = c->scene_gamma;
+    } else {
+        phong_dev = c->opt_x.p;
+    }
+    EvalRun er;
+    er.want_grad = false;
+    // K3 + K4 (+ image allreduce)
+    run_eval(c, st, r, er, phong_dev);
+    const double scale = 1.0 / (double)st->n_global;
+    CK(launch_scale(c->images.p, c->n_pix, scale, q, &c->launches));
+    CK(cudaMemsetAsync(c->loss.p, 0, 8, q));
+    CK(launch_loss_residual(c->images.p, c->opt_gt.p, c->n_pix, c->weights.p, c->loss.p, q, &c->launches));
+    // K5 with residual weights (+ gradient allreduce)
+    StoreView sv = st->view();
+    EvalArgs ea{};
+    ea.sp_t = c->sp_t.p;
+    ea.sp_ref = st->sp_ref.p;
+    ea.bt_tot = c->bt_tot.p;
+    ea.br_tot = st->br_tot.p;
+    ea.dbeta = c->dbeta.p;
+    ea.phong = phong_dev ? phong_dev : c->phong.p;
+    ea.images = c->images.p;
+    ea.clamps = c->clamps.p;
+    ea.weights = c->weights.p;
+    ea.g_span = c->g_span.p;
+    ea.g_vert = c->g_vert.p;
+    ea.g_phong = c->g_phong.p;
+    ea.do_beta = s.has_medium && s.unknown >= 0 ? 1 : 0;
+    CK(cudaEventRecord(c->ev[3], q));
+    CK(cudaMemsetAsync(c->g_span.p, 0, c->g_span.bytes(), q));
+    CK(cudaMemsetAsync(c->g_vert.p, 0, c->g_vert.bytes(), q));
+    CK(cudaMemsetAsync(c->g_phong.p, 0, 16, q));
+    CK(launch_gradient(s, sv, ea, q, &c->launches));
+    CK(cudaEventRecord(c->ev[4], q));
+    c->allreduce(c->g_span.p, c->g_span.n);
+    c->allreduce(c->g_vert.p, c->g_vert.n);
+    c->allreduce(c->g_phong.p, 2);
+    ++c->opt_t;
+    const double c1 = 1.0 - std::pow(c->adam.eta1, (double)c->opt_t);
+    const double c2 = 1.0 - std::pow(c->adam.eta2, (double)c->opt_t);
+    const double* g;
+    if (c->opt_mode == 0) {
+        CK(launch_combine_grad(c->g_span.p, c->g_vert.p, 1, c->V, scale, c->g_out.p, q, &c->launches));
+        g = c->g_out.p;
+    } else {
+        CK(launch_scale(c->g_phong.p, 2, scale, q, &c->launches));
+        g = c->g_phong.p;
+    }
+    CK(launch_adam(c->opt_x.p, c->opt_m1.p, c->opt_m2.p, g, c->opt_n, c->adam.alpha, c->adam.eta1,
+                   c->adam.eta2, c->adam.eps_guard, c1, c2, c->opt_step_scale.p, c->n_step_scale,
+                   c->opt_mode == 0 ? (c->adam.project_nonneg ? 0 : 2) : 1, q, &c->launches));
+    double loss = 0.0;
+    CK(cudaMemcpyAsync(&loss, c->loss.p, 8, cudaMemcpyDeviceToHost, q));
+    CK(cudaEventRecord(c->ev[5], q));
+    record_timings(c);
+    if (!std::isfinite(loss))
+        throw Err(PRC_ERR_NUMERIC, "reconstruct: non-finite loss at iteration " + std::to_string(c->opt_t - 1));
+    return loss;
+}
+
+PRC_EXPORT int prc_gpu_opt_init(prc_gpu_ctx* ctx, const prc_gpu_params* initial,
+                                const double* gt_images, const prc_gpu_adam_config* adam) {
+    if (!ctx || !gt_images) return fail(PRC_ERR_INVALID, "prc_gpu_opt_init: null argument");
+    ABI_TRY
+    begin(ctx);
+    ctx->check_scene();
+    opt_init(ctx, initial, gt_images, adam);
+    ABI_CATCH
+}
+
+PRC_EXPORT int prc_gpu_opt_step(prc_gpu_ctx* ctx, const prc_gpu_store* store, double* loss_out) {
+    if (!ctx || !store) return fail(PRC_ERR_INVALID, "prc_gpu_opt_step: null argument");
+    if (!ctx->opt_ready) return fail(PRC_ERR_INVALID, "prc_gpu_opt_step: optimizer not initialised");
+    ABI_TRY
+    begin(ctx);
+    const double l = opt_step(ctx, const_cast<prc_gpu_store*>(store));
+    if (loss_out) *loss_out = l;
+    ABI_CATCH
+}
+
+PRC_EXPORT int prc_gpu_opt_params(prc_gpu_ctx* ctx, double* beta_out, double* kappa_s, double* gamma) {
+    if (!ctx) return fail(PRC_ERR_INVALID, "prc_gpu_opt_params: null argument");
+    if (!ctx->opt_ready) return fail(PRC_ERR_INVALID, "optimizer not initialised");
+    ABI_TRY
+    begin(ctx);
+    if (ctx->opt_mode == 0) {
+        copy_out(ctx, beta_out, ctx->opt_x.p, (size_t)ctx->V);
+        if (kappa_s) *kappa_s = ctx->scene_kappa;
+        if (gamma) *gamma = ctx->scene_gamma;
+    } else {
+        double kg[2];
+        CK(cudaMemcpyAsync(kg, ctx->opt_x.p, 16, cudaMemcpyDeviceToHost, ctx->stream));
+        ctx->sync();
+        if (kappa_s) *kappa_s = kg[0];
+        if (gamma) *gamma = kg[1];
+    }
+    ctx->sync();
+    ABI_CATCH
+}
+
+PRC_EXPORT int prc_gpu_opt_images(prc_gpu_ctx* ctx, double* images_out) {
+    if (!ctx || !images_out) return fail(PRC_ERR_INVALID, "prc_gpu_opt_images: null argument");
+    ABI_TRY
+    begin(ctx);
+    copy_out(ctx, images_out, ctx->images.p, (size_t)ctx->n_pix);
+    ctx->sync();
+    ABI_CATCH
+}
+
+PRC_EXPORT int prc_gpu_reconstruct(prc_gpu_ctx* ctx, const prc_gpu_params* initial,
+                                   const double* gt_images, const prc_gpu_adam_config* adam,
+                                   const prc_gpu_reconstruct_opts* o, double* loss_history,
+                                   uint64_t* phases_out) {
+    if (!ctx || !gt_images || !o) return fail(PRC_ERR_INVALID, "prc_gpu_reconstruct: null argument");
+    if (o->n_paths == 0) return fail(PRC_ERR_CONFIG, "reconstruct: n_paths must be >= 1");
+    ABI_TRY
+    begin(ctx);
+    ctx->check_scene();
+    opt_init(ctx, initial, gt_images, adam);
+    const int n_r = std::max(1, o->recycle_period);
+    std::unique_ptr<prc_gpu_store> store;
+    uint64_t phases = 0;
+    for (int t = 0; t < o->max_iterations; ++t) {
+        if (t % n_r == 0) {  // resample + sort (inverse.cpp:175-204)
+            store.reset();
+            bind_trace_species(ctx);
+            double kg[2] = {ctx->scene_kappa, ctx->scene_gamma};
+            if (ctx->opt_mode == 1) {
+                CK(cudaMemcpyAsync(kg, ctx->opt_x.p, 16, cudaMemcpyDeviceToHost, ctx->stream));
+                ctx->sync();
+            }
+            prc_gpu_render_opts ro{o->n_paths, o->seed + 0x9E3779B97F4A7C15ull * (phases + 1),
+                                   o->max_bounces, -1};
+            store = trace_store(ctx, &ro, ctx->trace_sp.p, kg[0], kg[1], nullptr, true);
+            sort_store(ctx, store.get());
+            store->generation = (uint64_t)t;
+            ++phases;
+        }
+        const double l = opt_step(ctx, store.get());
+        if (loss_history) loss_history[t] = l;
+    }
+    if (phases_out) *phases_out = phases;
+    ABI_CATCH
+}
+
+PRC_EXPORT int prc_gpu_last_timings(const prc_gpu_ctx* ctx, double* ms6) {
+    if (!ctx || !ms6) return fail(PRC_ERR_INVALID, "null argument");
+    for (int i = 0; i < 6; ++i) ms6[i] = ctx->last_ms[i];
+    return PRC_OK;
+}
+
+PRC_EXPORT int prc_gpu_kernel_launches(const prc_gpu_ctx* ctx, uint64_t* out) {
+    if (!ctx || !out) return fail(PRC_ERR_INVALID, "null argument");
+    *out = ctx->launches;
+    return PRC_OK;
+}
+
+PRC_EXPORT int prc_gpu_debug_philox(prc_gpu_ctx* ctx, uint64_t seed, uint64_t stream, uint64_t n,
+                                    uint32_t* out) {
+    if (!ctx || !out) return fail(PRC_ERR_INVALID, "null argument");
+    ABI_TRY
+    begin(ctx);
+    DBuf<uint32_t> d;
+    d.alloc(std::max<uint64_t>(n, 1));
+    CK(launch_philox(seed, stream, n, d.p, ctx->stream, &ctx->launches));
+    if (n) CK(cudaMemcpyAsync(out, d.p, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+    ABI_CATCH
+}
+
+PRC_EXPORT int prc_gpu_debug_walk(prc_gpu_ctx* ctx, uint64_t n, const double* rays,
+                                  uint32_t* counts_out, uint32_t* voxels_out, double* lengths_out,
+                                  uint64_t cap) {
+    if (!ctx || !rays || !counts_out) return fail(PRC_ERR_INVALID, "null argument");
+    ABI_TRY
+    begin(ctx);
+    ctx->check_scene();
+    if (!ctx->dsc.has_medium) throw Err(PRC_ERR_CONFIG, "scene has no medium grid");
+    cudaStream_t q = ctx->stream;
+    DBuf<double> dr;
+    DBuf<uint32_t> dc;
+    dr.alloc(std::max<uint64_t>(7 * n, 1));
+    dc.alloc(std::max<uint64_t>(n, 1));
+    if (n) CK(cudaMemcpyAsync(dr.p, rays, 7 * n * 8, cudaMemcpyHostToDevice, q));
+    CK(launch_walk(ctx->dsc, dr.p, (long long)n, dc.p, nullptr, nullptr, nullptr, q, &ctx->launches));
+    if (n) CK(cudaMemcpyAsync(counts_out, dc.p, n * 4, cudaMemcpyDeviceToHost, q));
+    ctx->sync();
+    if (voxels_out && lengths_out) {
+        std::vector<unsigned long long> off(n + 1, 0);
+        for (uint64_t i = 0; i < n; ++i) off[i + 1] = off[i] + counts_out[i];
+        if (off[n] > cap) throw Err(PRC_ERR_INVALID, "debug_walk: capacity too small");
+        DBuf<unsigned long long> doff;
+        DBuf<uint32_t> dv;
+        DBuf<double> dl;
+        doff.alloc(std::max<uint64_t>(n, 1));
+        dv.alloc(std::max<unsigned long long>(off[n], 1));
+        dl.alloc(std::max<unsigned long long>(off[n], 1));
+        if (n) CK(cudaMemcpyAsync(doff.p, off.data(), n * 8, cudaMemcpyHostToDevice, q));
+        CK(launch_walk(ctx->dsc, dr.p, (long long)n, dc.p, doff.p, dv.p, dl.p, q, &ctx->launches));
+        if (off[n]) {
+            CK(cudaMemcpyAsync(voxels_out, dv.p, off[n] * 4, cudaMemcpyDeviceToHost, q));
+            CK(cudaMemcpyAsync(lengths_out, dl.p, off[n] * 8, cudaMemcpyDeviceToHost, q));
+        }
+        ctx->sync();
+    }
+    ABI_CATCH
+}
+
+PRC_EXPORT int prc_gpu_debug_pixel_of(prc_gpu_ctx* ctx, int det, uint64_t n, const double* pts,
+                                      int32_t* out) {
+    if (!ctx || !pts || !out) return fail(PRC_ERR_INVALID, "null argument");
+    ABI_TRY
+    begin(ctx);
+    ctx->check_scene();
+    if (det < 0 || det >= ctx->dsc.n_det) throw Err(PRC_ERR_INVALID, "detector index out of range");
+    cudaStream_t q = ctx->stream;
+    DBuf<double> dp;
+    DBuf<int32_t> dout;
+    dp.alloc(std::max<uint64_t>(3 * n, 1));
+    dout.alloc(std::max<uint64_t>(n, 1));
+    if (n) CK(cudaMemcpyAsync(dp.p, pts, 3 * n * 8, cudaMemcpyHostToDevice, q));
+    CK(launch_pixel_of(ctx->dsc, det, dp.p, (long long)n, dout.p, q, &ctx->launches));
+    if (n) CK(cudaMemcpyAsync(out, dout.p, n * 4, cudaMemcpyDeviceToHost, q));
+    ctx->sync();
+    ABI_CATCH
+}

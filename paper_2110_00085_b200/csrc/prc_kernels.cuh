@@ -1,0 +1,141 @@
+// prc_kernels.cuh — kernel argument blocks and host-side launchers (prc_kernels.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "prc_device.cuh"
+
+// Device path store in structure-of-arrays form.  Record (p, b) = vertex b of the path
+// in storage position p lives at rec_base[p] + b * stride[p]; its event-cache slot
+// (interaction vertices b = 1..B-1) at iv_base[p] + (b - 1) * stride[p].  After the
+// trace the layout is path-major (stride 1); after sort_by_size it is bucket-major
+// (paths of equal B interleaved, stride = bucket population) so that a warp of 32
+// consecutive sorted paths reads each field of vertex b with one coalesced request.
+struct StoreView {
+    unsigned long long n;
+    const uint32_t* B;
+    const unsigned long long* rec_base;
+    const uint32_t* stride;
+    const unsigned long long* iv_base;
+    const double *px, *py, *pz, *dx, *dy, *dz, *tt, *ct;
+    const int32_t* vox;
+    const uint32_t* meta;
+    unsigned long long n_iv;
+    float* ev_val;    // [det][iv]: cached event value (K4 -> K5)
+    int32_t* ev_pix;  // [det][iv]: pixel, -1 when no event
+};
+
+struct RecordsOut {
+    double *px, *py, *pz, *dx, *dy, *dz, *tt, *ct;
+    int32_t* vox;
+    uint32_t* meta;
+};
+
+struct EvalArgs {
+    const float* sp_t;    // n_species x V, extinction under the evaluated parameters
+    const float* sp_ref;  // n_species x V, extinction the paths were sampled under
+    const float* bt_tot;  // V
+    const float* br_tot;  // V
+    const float* dbeta;   // V: bt_tot - br_tot (computed in fp64, stored fp32)
+    const double* phong;  // [kappa_s, gamma] bound to the target surface
+    double* images;       // raw (un-normalised) pixel sums
+    unsigned long long* clamps;
+    const double* weights;  // pixel weights (residuals), NULL = 1
+    double* g_span;         // V: transmittance part of dL/dbeta, shared by all species
+    double* g_vert;         // n_vert_out x V: vertex score parts
+    double* g_phong;        // [d kappa, d gamma]
+    int per_species, legacy, do_beta;
+};
+
+struct TraceArgs {
+    const double* beta_tot;  // V, fp64 total extinction (sampling point)
+    const double* sp_beta;   // n_species x V, fp64
+    unsigned long long seed, stream_base, n;
+    int max_bounces, max_events;
+    uint32_t* B;
+    uint8_t* trunc;
+    int* err;
+    const unsigned long long* off;  // write pass: record offset of each path
+    RecordsOut rec;
+};
+
+// ---- launchers (return cudaError_t); `launches` counts kernels issued -------------
+cudaError_t launch_trace(const DScene& sc, const TraceArgs& a, bool write, cudaStream_t s,
+                         unsigned long long* launches);
+cudaError_t launch_prep(int n_species, long long V, const double* const* src_t,
+                        const double* br_tot64, float* sp_t, float* bt_tot, float* dbeta,
+                        cudaStream_t s, unsigned long long* launches);
+cudaError_t launch_prep_ref(int n_species, long long V, const double* const* src_ref,
+                            double* br_tot64, float* sp_ref, float* br_tot, double* beta_tot64,
+                            cudaStream_t s, unsigned long long* launches);
+cudaError_t launch_forward(const DScene& sc, const StoreView& st, const EvalArgs& ea,
+                           cudaStream_t s, unsigned long long* launches);
+cudaError_t launch_gradient(const DScene& sc, const StoreView& st, const EvalArgs& ea,
+                            cudaStream_t s, unsigned long long* launches);
+cudaError_t launch_scale(double* x, long long n, double scale, cudaStream_t s,
+                         unsigned long long* launches);
+cudaError_t launch_combine_grad(const double* g_span, const double* g_vert, int n_out, long long V,
+                                double scale, double* out, cudaStream_t s,
+                                unsigned long long* launches);
+cudaError_t launch_loss_residual(const double* F, const double* gt, long long n, double* residual,
+                                 double* loss, cudaStream_t s, unsigned long long* launches);
+cudaError_t launch_adam(double* x, double* m1, double* m2, const double* g, long long n,
+                        double alpha, double eta1, double eta2, double eps, double c1, double c2,
+                        const double* step_scale, int n_step_scale, int mode, cudaStream_t s,
+                        unsigned long long* launches);
+cudaError_t launch_set_species(int n_species, long long V, int unknown, const double* scene_sp,
+                               const double* beta_unknown, double* out, cudaStream_t s,
+                               unsigned long long* launches);
+
+// Exclusive scan of n uint64 values (CUB).  tmp is grown as needed.
+cudaError_t scan_u64(const unsigned long long* in, unsigned long long* out, long long n,
+                     void** tmp, size_t* tmp_bytes, cudaStream_t s);
+cudaError_t launch_size_terms(const uint32_t* B, long long n, unsigned long long* rec_terms,
+                              unsigned long long* iv_terms, cudaStream_t s,
+                              unsigned long long* launches);
+cudaError_t launch_path_major_layout(const unsigned long long* rec_off,
+                                     const unsigned long long* iv_off, long long n,
+                                     unsigned long long* rec_base, uint32_t* stride,
+                                     unsigned long long* iv_base, cudaStream_t s,
+                                     unsigned long long* launches);
+cudaError_t reduce_max_u32(const uint32_t* in, long long n, uint32_t* out_dev, void** tmp,
+                           size_t* tmp_bytes, cudaStream_t s);
+
+// ---- K2 stable counting sort by B ------------------------------------------------
+// tile_hist: nb * n_tiles counters (bin-major).  perm[dest] = source position.
+cudaError_t launch_sort_hist(const uint32_t* B, long long n, int nb, int tile,
+                             unsigned long long* tile_hist, cudaStream_t s,
+                             unsigned long long* launches);
+cudaError_t launch_sort_rank(const uint32_t* B, long long n, int nb, int tile,
+                             const unsigned long long* tile_off, uint32_t* perm,
+                             cudaStream_t s, unsigned long long* launches);
+// Builds the bucket-major layout of sorted path i from the bucket table.
+cudaError_t launch_bucket_layout(const uint32_t* perm, const uint32_t* B_old,
+                                 const unsigned long long* stream_old, const uint8_t* trunc_old,
+                                 long long n, const unsigned long long* bucket_start,
+                                 const unsigned long long* bucket_rec,
+                                 const unsigned long long* bucket_iv, uint32_t* B_new,
+                                 unsigned long long* stream_new, uint8_t* trunc_new,
+                                 unsigned long long* rec_base, uint32_t* stride,
+                                 unsigned long long* iv_base, cudaStream_t s,
+                                 unsigned long long* launches);
+cudaError_t launch_gather_records(const StoreView& old_st, const uint32_t* perm, long long n,
+                                  const unsigned long long* rec_base_new,
+                                  const uint32_t* stride_new, const RecordsOut& out,
+                                  cudaStream_t s, unsigned long long* launches);
+
+// ---- diagnostics / export ----------------------------------------------------------
+cudaError_t launch_philox(unsigned long long seed, unsigned long long stream,
+                          unsigned long long n, uint32_t* out, cudaStream_t s,
+                          unsigned long long* launches);
+cudaError_t launch_walk(const DScene& sc, const double* rays, long long n, uint32_t* counts,
+                        const unsigned long long* offsets, uint32_t* vox, double* len,
+                        cudaStream_t s, unsigned long long* launches);
+cudaError_t launch_pixel_of(const DScene& sc, int det, const double* pts, long long n,
+                            int32_t* out, cudaStream_t s, unsigned long long* launches);
+// Per (interaction vertex, detector) event materialisation: valid, pixel, cos_le,
+// geom and the LE ray (origin is the vertex; w xyz, r) — slot layout as the cache.
+cudaError_t launch_events(const DScene& sc, const StoreView& st, int32_t* pix, double* cos_le,
+                          double* geom, double* ray_w, cudaStream_t s,
+                          unsigned long long* launches);

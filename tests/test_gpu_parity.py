@@ -1,0 +1,323 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the CPU oracle and the
+reference's golden vectors.
+
+Tolerances (north_star): images and gradients within 1e-5 relative on identical stored
+path sets; sort order, voxel indexing (DDA spans incl. length bits) and pixel indices
+bit-exact; fresh Monte-Carlo sampling within stated statistical tolerances.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+from paper_2110_00085_b200 import abi
+from paper_2110_00085_b200 import scene as S
+from paper_2110_00085_b200.gpu import EvalOptions, PrcConfigError, PrcIOError, RenderOptions
+from tests.fixtures import FIXTURES, golden, perturbed, weight_patterns
+
+pytestmark = pytest.mark.gpu
+
+IMG_TOL = 1e-5   # max_p |g - r| / max(|r_p|, 1e-3 max|r|)
+GRAD_TOL = 1e-5  # |g - r| <= 1e-5 max(|g|, |r|, max_v |r_v|)
+
+
+def img_err(a, r):
+    floor = 1e-3 * max(np.abs(r).max(), 1e-300)
+    return float((np.abs(a - r) / np.maximum(np.abs(r), floor)).max()) if r.size else 0.0
+
+
+def grad_err(a, r):
+    if r.size == 0:
+        return 0.0
+    scale = max(np.abs(r).max(), 1e-300)
+    return float((np.abs(a - r) / np.maximum(np.maximum(np.abs(a), np.abs(r)), scale)).max())
+
+
+def scalar_err(a, r):
+    return abs(a - r) / max(abs(a), abs(r), 1e-300)
+
+
+# ---------------------------------------------------------------- bit-exact primitives
+def test_philox_device_matches_reference(ctx):
+    g = golden("common")
+    assert [hex(x) for x in ctx.debug_philox(0, 0, 4)] == ["0x6627e8d5", "0xe169c58d", "0xbc57ac4c", "0x9b00dbd8"]
+    for k, v in g.items():
+        if k.startswith("philox_"):
+            _, seed, stream = k.split("_")
+            assert np.array_equal(ctx.debug_philox(int(seed), int(stream), v.size), v)
+
+
+@pytest.mark.parametrize("name", ["tomo2", "cloud", "mixed"])
+def test_device_dda_bit_exact(ctx, port, name):
+    g = golden("common")
+    scene = FIXTURES[name]["scene"]()
+    ctx.upload(scene)
+    c, v, ln = ctx.debug_walk(g[f"walk_{name}_rays"])
+    assert np.array_equal(c, g[f"walk_{name}_counts"])
+    assert np.array_equal(v, g[f"walk_{name}_vox"])
+    assert np.array_equal(ln.view(np.uint64), g[f"walk_{name}_len"].view(np.uint64))
+    # LE-style rays from interior points toward every camera of the bench scene (128^3)
+    big = S.cloud_scene(128, 16, 16)
+    ctx.upload(big)
+    rng = np.random.default_rng(3)
+    x = rng.uniform(0.05, 0.95, size=(3000, 3))
+    rays = []
+    for d in big.detectors:
+        to = np.asarray(d.position) - x
+        r = np.linalg.norm(to, axis=1)
+        w = to * (1.0 / r)[:, None]
+        rays.append(np.concatenate([x, w, r[:, None]], axis=1))
+    rays = np.concatenate(rays)
+    c1, v1, l1 = ctx.debug_walk(rays)
+    c2, v2, l2 = port.walk(big, rays)
+    assert np.array_equal(c1, c2) and np.array_equal(v1, v2)
+    assert np.array_equal(l1.view(np.uint64), l2.view(np.uint64))
+
+
+@pytest.mark.parametrize("name", ["tomo2", "cloud", "mixed"])
+def test_device_pixel_of_bit_exact(ctx, name):
+    g = golden("common")
+    scene = FIXTURES[name]["scene"]()
+    ctx.upload(scene)
+    pts = g[f"pixel_{name}_pts"]
+    for k in range(len(scene.detectors)):
+        assert np.array_equal(ctx.debug_pixel_of(k, pts), g[f"pixel_{name}_{k}"])
+
+
+# ---------------------------------------------------------------- K2 sort
+@pytest.mark.parametrize("name", list(FIXTURES))
+def test_sort_permutation_bit_exact(ctx, golden_dir, name):
+    scene = FIXTURES[name]["scene"]()
+    ctx.upload(scene)
+    st = ctx.load_store(str(golden_dir / f"{name}.pstr"))
+    assert not st.sorted_flag
+    ctx.sort_by_size(st)
+    assert st.sorted_flag
+    assert np.array_equal(st.streams(), golden(name)["sorted_streams"])
+    # idempotent (stable)
+    before = st.streams()
+    ctx.sort_by_size(st)
+    assert np.array_equal(st.streams(), before)
+
+
+def test_sort_large_random_sizes_match_stable_sort(ctx, port):
+    scene = S.cloud_scene(16, 8, 8)
+    ctx.upload(scene)
+    st = ctx.render(scene, RenderOptions(n_paths=300_000, seed=5, keep_paths=True)).store
+    sizes = st.sizes()
+    ctx.sort_by_size(st)
+    expect = np.argsort(sizes, kind="stable").astype(np.uint64)
+    assert np.array_equal(st.streams(), expect)
+    assert np.array_equal(st.sizes(), np.sort(sizes, kind="stable"))
+
+
+def test_sort_empty_store_rejected(ctx):
+    with pytest.raises(PrcConfigError):
+        ctx.render(FIXTURES["cloud"]["scene"](), RenderOptions(n_paths=0))
+
+
+# ---------------------------------------------------------------- K4/K5 on identical stores
+@pytest.mark.parametrize("name", list(FIXTURES))
+@pytest.mark.parametrize("sort", [False, True])
+def test_evaluate_matches_reference_on_its_store(ctx, golden_dir, name, sort):
+    scene = FIXTURES[name]["scene"]()
+    g = golden(name)
+    ctx.upload(scene)
+    st = ctx.load_store(str(golden_dir / f"{name}.pstr"))
+    if sort:
+        ctx.sort_by_size(st)
+    worst = [0.0, 0.0]
+    for tag, params in (("ref", None), ("pert", perturbed(scene))):
+        for wtag, w in weight_patterns(scene).items():
+            r = ctx.evaluate_store(scene, st, params, EvalOptions(want_grad=True, pixel_weights=w))
+            e_img = img_err(r.images, g[f"{tag}_{wtag}_images"])
+            assert e_img <= IMG_TOL, (tag, wtag, e_img)
+            worst[0] = max(worst[0], e_img)
+            if scene.unknown_species() >= 0:
+                e_g = grad_err(r.grad_beta, g[f"{tag}_{wtag}_grad"])
+                assert e_g <= GRAD_TOL, (tag, wtag, e_g)
+                worst[1] = max(worst[1], e_g)
+            else:
+                assert scalar_err(r.grad_kappa, float(g[f"{tag}_{wtag}_gk"])) <= GRAD_TOL
+                assert scalar_err(r.grad_gamma, float(g[f"{tag}_{wtag}_gg"])) <= GRAD_TOL
+            assert r.clamp_events == int(g[f"{tag}_{wtag}_clamps"])
+        if scene.unknown_species() >= 0:
+            r = ctx.evaluate_store(scene, st, params, EvalOptions(want_grad=True, legacy_score=True))
+            assert grad_err(r.grad_beta, g[f"{tag}_legacy_grad"]) <= GRAD_TOL
+    print(f"{name} sort={sort}: max image rel err {worst[0]:.2e}, max grad rel err {worst[1]:.2e}")
+
+
+def test_per_type_gradients(ctx, golden_dir):
+    """Config (c): both species' gradients from one pass; each equals the reference's
+    single-unknown gradient with that species flagged (SURVEY a15 flip oracle)."""
+    scene = FIXTURES["tomo2"]["scene"]()
+    flip = FIXTURES["tomo2"]["flip_unknown"]()
+    g = golden("tomo2")
+    ctx.upload(scene)
+    st = ctx.load_store(str(golden_dir / "tomo2.pstr"))
+    w = weight_patterns(scene)["w"]
+    p0 = perturbed(scene)  # species 0 perturbed
+    r = ctx.evaluate_store(scene, st, S.ParamSet(species_beta=[p0.beta, None]),
+                           EvalOptions(want_grad=True, pixel_weights=w, per_species=True))
+    assert grad_err(r.grad_beta[0], g["pert_w_grad"]) <= GRAD_TOL
+    p1 = perturbed(flip)  # species 1 perturbed
+    r = ctx.evaluate_store(scene, st, S.ParamSet(species_beta=[None, p1.beta]),
+                           EvalOptions(want_grad=True, pixel_weights=w, per_species=True))
+    assert img_err(r.images, g["flip_pert_w_images"]) <= IMG_TOL
+    assert grad_err(r.grad_beta[1], g["flip_pert_w_grad"]) <= GRAD_TOL
+
+
+def test_self_normalize_rejected(ctx, golden_dir):
+    scene = FIXTURES["tomo2"]["scene"]()
+    ctx.upload(scene)
+    st = ctx.load_store(str(golden_dir / "tomo2.pstr"))
+    with pytest.raises(PrcConfigError):
+        ctx.evaluate_store(scene, st, None, EvalOptions(self_normalize=True))
+
+
+def test_pstr_errors(ctx, tmp_path):
+    ctx.upload(FIXTURES["tomo2"]["scene"]())
+    p = tmp_path / "bad.pstr"
+    p.write_bytes(b"XXXX????")
+    with pytest.raises(PrcIOError, match="bad magic"):
+        ctx.load_store(str(p))
+    with pytest.raises(PrcIOError):
+        ctx.load_store(str(tmp_path / "no_such_file.pstr"))
+
+
+# ---------------------------------------------------------------- K1 trace
+@pytest.mark.parametrize("name", list(FIXTURES))
+def test_device_store_round_trip_through_reference_format(ctx, port, tmp_path, name):
+    """GPU-traced store -> PSTR (spans/events materialised on the device) -> oracle
+    evaluates the identical stored path set; GPU evaluation agrees within 1e-5."""
+    fx = FIXTURES[name]
+    scene = fx["scene"]()
+    ctx.upload(scene)
+    rr = ctx.render(scene, RenderOptions(n_paths=fx["n"], seed=11, keep_paths=True,
+                                         max_bounces=fx.get("max_bounces", 500)))
+    st = rr.store
+    ctx.sort_by_size(st)
+    path = str(tmp_path / "gpu.pstr")
+    st.save(path)
+    ost = port.load(path)
+    assert np.array_equal(ost.streams(), st.streams())
+    assert np.array_equal(ost.sizes(), st.sizes())
+    for params in (None, perturbed(scene)):
+        w = weight_patterns(scene)["res"]
+        a = ctx.evaluate_store(scene, st, params, EvalOptions(want_grad=True, pixel_weights=w))
+        b = port.evaluate(scene, ost, params, abi.PRC_EVAL_NORMALIZE | abi.PRC_EVAL_WANT_GRAD, w)
+        assert img_err(a.images, b["images"]) <= IMG_TOL
+        if scene.unknown_species() >= 0:
+            assert grad_err(a.grad_beta, b["grad"]) <= GRAD_TOL
+        else:
+            assert scalar_err(a.grad_kappa, b["grad_kappa"]) <= GRAD_TOL
+    # fresh image == evaluation at the sampling point
+    assert img_err(ctx.recycled_render(scene, st, None), rr.images) <= 1e-12
+
+
+@pytest.mark.parametrize("name", list(FIXTURES))
+def test_fresh_paths_follow_the_reference_sampler(ctx, port, name):
+    """Same (seed, stream) Philox streams: device paths coincide with the reference's
+    except where CUDA libm (log1p/sin/cos/cbrt/pow) rounds differently; the path-size
+    histogram and the fresh image agree statistically."""
+    fx = FIXTURES[name]
+    scene = fx["scene"]()
+    n = 4000
+    mb = fx.get("max_bounces", 500)
+    ctx.upload(scene)
+    rr = ctx.render(scene, RenderOptions(n_paths=n, seed=21, keep_paths=True, max_bounces=mb))
+    img_o, tr_o, st_o = port.render(scene, n, 21, max_bounces=mb)
+    same = (rr.store.sizes() == st_o.sizes()).mean()
+    assert same >= 0.97, same
+    # image totals within 4 combined standard errors (per-path contributions)
+    assert abs(rr.images.sum() - img_o.sum()) <= 0.02 * img_o.sum() + 1e-12
+
+
+def test_truncation_and_event_cap(ctx):
+    s = S.homogeneous_cube(80.0, 1.0, "rayleigh")
+    ctx.upload(s)
+    r = ctx.render(s, RenderOptions(n_paths=50, seed=3, max_bounces=2, keep_paths=True))
+    assert r.truncated_paths > 0 and r.store.info()["truncated"] == r.truncated_paths
+    s = S.homogeneous_cube(50.0, 0.9, "rayleigh")
+    ctx.upload(s)
+    r = ctx.render(s, RenderOptions(n_paths=200, seed=1, max_bounces=1000, max_scatter_events=1,
+                                    keep_paths=True))
+    assert r.truncated_paths == 0 and r.store.sizes().max() <= 2
+    v = S.homogeneous_cube(0.0, 0.9)
+    ctx.upload(v)
+    r = ctx.render(v, RenderOptions(n_paths=500, seed=1))
+    assert (r.images == 0).all() and r.truncated_paths == 0
+
+
+def test_unbiased_recycling_against_fresh(ctx):
+    """test_pathstore.cpp:152-170: recycled estimate at +15% tracks a fresh render."""
+    s = S.two_species_cube(np.full(64, 4.0), 4, 0.04, 4, 4)
+    ctx.upload(s)
+    st = ctx.render(s, RenderOptions(n_paths=400_000, seed=29, keep_paths=True)).store
+    t = S.ParamSet(np.full(64, 4.0 * 1.15))
+    rec = ctx.recycled_render(s, st, t)
+    s2 = S.two_species_cube(np.full(64, 4.0 * 1.15), 4, 0.04, 4, 4)
+    ctx.upload(s2)
+    fresh = ctx.render(s2, RenderOptions(n_paths=400_000, seed=877)).images
+    assert np.abs(rec - fresh).sum() / fresh.sum() < 0.02
+
+
+# ---------------------------------------------------------------- Algorithm 2
+def test_adam_step_matches_restatement(ctx, golden_dir):
+    """One device-resident iteration (K3-K6) vs numpy ADAM on the reference gradient."""
+    scene = FIXTURES["tomo2"]["scene"]()
+    g = golden("tomo2")
+    ctx.upload(scene)
+    st = ctx.load_store(str(golden_dir / "tomo2.pstr"))
+    t = perturbed(scene)
+    # gt such that residual = F_t - gt = "res" weights of the golden set
+    Ft = g["pert_res_images"]
+    res = weight_patterns(scene)["res"]
+    gt = Ft - res
+    alpha = 0.05
+    ctx.opt_init(t, gt, alpha=alpha)
+    loss = ctx.opt_step(st)
+    assert abs(loss - 0.5 * (res ** 2).sum()) <= 1e-5 * loss
+    grad = g["pert_res_grad"]
+    m1 = 0.1 * grad
+    m2 = 0.001 * grad * grad
+    mhat, vhat = m1 / (1 - 0.9), m2 / (1 - 0.999)
+    expect = np.maximum(t.beta - alpha * mhat / (np.sqrt(vhat) + 1e-8), 0.0)
+    got = ctx.opt_params().beta
+    # first ADAM step is alpha * g / (|g| + eps): a gradient error dg moves it by at most
+    # alpha * 2 dg / (|g| + eps); dg is bounded by the 1e-5 scale-relative gradient bar.
+    dg = GRAD_TOL * np.abs(grad).max()
+    allow = alpha * 2.0 * dg / (np.abs(grad) + 1e-8) + 1e-12
+    assert (np.abs(got - expect) <= allow).all()
+
+
+def test_reconstruct_loop_runs_algorithm2(ctx, ref):
+    """Algorithm 2 on the device: resample + sort every N_r, recycle otherwise; loss
+    falls like the reference's loop on the same problem."""
+    s = S.cloud_scene(8, 8, 8)
+    truth = s.species[0].extinction.copy()
+    ctx.upload(s)
+    gt = ctx.render(s, RenderOptions(n_paths=200_000, seed=611)).images
+    init = S.ParamSet(np.full(truth.size, truth.mean()))
+    out = ctx.reconstruct(s, gt, init, n_paths=20_000, seed=271, recycle_period=10,
+                          max_iterations=40, alpha=0.3)
+    assert out["sampling_phases"] == 4
+    loss = out["loss"]
+    assert np.isfinite(loss).all() and loss[-1] < 0.5 * loss[0]
+    r = ref.reconstruct(s, init, gt, alpha=0.3, seed=271, n_paths=20_000, recycle_period=10,
+                        max_iterations=40, workers=os.cpu_count() or 1)
+    assert r["sampling_phases"] == 4
+    assert loss[-1] <= 2.0 * r["loss"][-1] + 1e-12 and r["loss"][-1] <= 2.0 * loss[-1] + 1e-12
+
+
+def test_phong_reconstruct_moves_toward_truth(ctx):
+    s = S.phong_box(0.7, 50.0, 16, 16, 0.3)
+    ctx.upload(s)
+    gt = ctx.render(s, RenderOptions(n_paths=400_000, seed=501, max_bounces=40)).images
+    out = ctx.reconstruct(s, gt, S.ParamSet(None, 0.4, 25.0), n_paths=100_000, seed=733,
+                          recycle_period=10, max_iterations=60, max_bounces=40, alpha=0.008,
+                          step_scale=[2.0, 100.0])
+    p = out["params"]
+    assert abs(p.kappa_s - 0.7) < abs(0.4 - 0.7) and abs(p.gamma - 50.0) < abs(25.0 - 50.0)
+    assert out["loss"][-1] < out["loss"][0]
