@@ -279,6 +279,12 @@ int prc_gpu_reconstruct(prc_gpu_ctx* ctx, const prc_gpu_params* initial, const d
  * events on the launching stream: [0] prep, [1] forward (K4), [2] image allreduce +
  * loss, [3] gradient (K5), [4] grad allreduce + ADAM, [5] total. */
 int prc_gpu_last_timings(const prc_gpu_ctx* ctx, double* ms6);
+/* CUDA events recorded on the context's stream: start / stop -> elapsed ms. */
+int prc_gpu_timer_start(prc_gpu_ctx* ctx);
+int prc_gpu_timer_stop(prc_gpu_ctx* ctx, double* ms);
+/* Device counting pass over a store (no gathers): out[0] events, out[1] live path-span
+ * incidences (segments 1..B-1), out[2] LE span incidences, out[3] all path spans. */
+int prc_gpu_store_stats(prc_gpu_ctx* ctx, const prc_gpu_store* store, uint64_t* out4);
 /* Number of kernels this library launched since ctx creation. */
 int prc_gpu_kernel_launches(const prc_gpu_ctx* ctx, uint64_t* out);
 

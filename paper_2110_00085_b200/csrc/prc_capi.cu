@@ -131,9 +131,12 @@ struct prc_gpu_ctx {
     int n_step_scale = 0;
     // timing
     cudaEvent_t ev[6] = {};
+    cudaEvent_t timer[2] = {};
     double last_ms[6] = {};
     ~prc_gpu_ctx() {
         if (cub_tmp) cudaFree(cub_tmp);
+        for (auto& e : timer)
+            if (e) cudaEventDestroy(e);
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
         if (comm) ncclCommDestroy(comm);
@@ -1519,6 +1522,46 @@ PRC_EXPORT int prc_gpu_last_timings(const prc_gpu_ctx* ctx, double* ms6) {
     if (!ctx || !ms6) return fail(PRC_ERR_INVALID, "null argument");
     for (int i = 0; i < 6; ++i) ms6[i] = ctx->last_ms[i];
     return PRC_OK;
+}
+
+PRC_EXPORT int prc_gpu_timer_start(prc_gpu_ctx* ctx) {
+    if (!ctx) return fail(PRC_ERR_INVALID, "null argument");
+    ABI_TRY
+    begin(ctx);
+    if (!ctx->timer[0]) {
+        CK(cudaEventCreate(&ctx->timer[0]));
+        CK(cudaEventCreate(&ctx->timer[1]));
+    }
+    CK(cudaEventRecord(ctx->timer[0], ctx->stream));
+    ABI_CATCH
+}
+
+PRC_EXPORT int prc_gpu_timer_stop(prc_gpu_ctx* ctx, double* ms) {
+    if (!ctx || !ms || !ctx->timer[0]) return fail(PRC_ERR_INVALID, "timer not started");
+    ABI_TRY
+    begin(ctx);
+    CK(cudaEventRecord(ctx->timer[1], ctx->stream));
+    CK(cudaEventSynchronize(ctx->timer[1]));
+    float f = 0.f;
+    CK(cudaEventElapsedTime(&f, ctx->timer[0], ctx->timer[1]));
+    *ms = f;
+    ABI_CATCH
+}
+
+PRC_EXPORT int prc_gpu_store_stats(prc_gpu_ctx* ctx, const prc_gpu_store* store, uint64_t* out4) {
+    if (!ctx || !store || !out4) return fail(PRC_ERR_INVALID, "null argument");
+    ABI_TRY
+    begin(ctx);
+    ctx->check_scene();
+    DBuf<unsigned long long> d;
+    d.alloc(4);
+    CK(cudaMemsetAsync(d.p, 0, 32, ctx->stream));
+    CK(launch_stats(ctx->dsc, const_cast<prc_gpu_store*>(store)->view(), d.p, ctx->stream,
+                    &ctx->launches));
+    ctx->allreduce_u64(d.p, 4);
+    CK(cudaMemcpyAsync(out4, d.p, 32, cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+    ABI_CATCH
 }
 
 PRC_EXPORT int prc_gpu_kernel_launches(const prc_gpu_ctx* ctx, uint64_t* out) {

@@ -767,6 +767,60 @@ __global__ void k_events(const __grid_constant__ DScene sc, const __grid_constan
     }
 }
 
+__global__ void __launch_bounds__(kTPB) k_stats(const __grid_constant__ DScene sc,
+                                                const __grid_constant__ StoreView st,
+                                                unsigned long long* out) {
+    const long long p = path_index(st.n);
+    unsigned long long ev = 0, live = 0, le = 0, all = 0;
+    if (p >= 0) {
+        const int B = (int)st.B[p];
+        const unsigned long long rb = st.rec_base[p];
+        const unsigned rs = st.stride[p];
+        V3 xprev = mk(st.px[rb], st.py[rb], st.pz[rb]);
+        for (int b = 1; b <= B; ++b) {
+            const Rec R = load_rec(st, rb + (unsigned long long)b * rs);
+            unsigned long long c = 0;
+            if (sc.has_medium)
+                dda_walk(sc, xprev, R.d, R.t, [&](int, double, double) {
+                    ++c;
+                    return true;
+                });
+            all += c;
+            if (b < B) {
+                live += c;
+                for (int k = 0; k < sc.n_det; ++k) {
+                    const DDet& D = sc.det[k];
+                    if (pixel_of(D, R.x) < 0) continue;
+                    V3 w;
+                    double r, geom, cos_le;
+                    if (!event_geometry(sc, D, R.x, R.d, meta_kind(R.meta), meta_surface(R.meta), w, r,
+                                        geom, cos_le))
+                        continue;
+                    ++ev;
+                    if (sc.has_medium)
+                        dda_walk(sc, R.x, w, r, [&](int, double, double) {
+                            ++le;
+                            return true;
+                        });
+                }
+            }
+            xprev = R.x;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        ev += __shfl_down_sync(0xffffffffu, ev, o);
+        live += __shfl_down_sync(0xffffffffu, live, o);
+        le += __shfl_down_sync(0xffffffffu, le, o);
+        all += __shfl_down_sync(0xffffffffu, all, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(out, ev);
+        atomicAdd(out + 1, live);
+        atomicAdd(out + 2, le);
+        atomicAdd(out + 3, all);
+    }
+}
+
 }  // namespace
 
 // ============================================================================ launchers
@@ -974,6 +1028,13 @@ cudaError_t launch_pixel_of(const DScene& sc, int det, const double* pts, long l
                             cudaStream_t s, unsigned long long* launches) {
     if (n == 0) return cudaSuccess;
     k_pixel_of<<<grid_for(n), kTPB, 0, s>>>(sc, det, pts, n, out);
+    LAUNCH_DONE();
+}
+
+cudaError_t launch_stats(const DScene& sc, const StoreView& st, unsigned long long* out,
+                         cudaStream_t s, unsigned long long* launches) {
+    if (st.n == 0) return cudaSuccess;
+    k_stats<<<grid_for((long long)st.n), kTPB, 0, s>>>(sc, st, out);
     LAUNCH_DONE();
 }
 

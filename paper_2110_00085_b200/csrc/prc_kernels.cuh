@@ -136,6 +136,9 @@ cudaError_t launch_pixel_of(const DScene& sc, int det, const double* pts, long l
                             int32_t* out, cudaStream_t s, unsigned long long* launches);
 // Per (interaction vertex, detector) event materialisation: valid, pixel, cos_le,
 // geom and the LE ray (origin is the vertex; w xyz, r) — slot layout as the cache.
+// Counting pass: out[0] events, [1] live path spans, [2] LE spans, [3] all path spans.
+cudaError_t launch_stats(const DScene& sc, const StoreView& st, unsigned long long* out,
+                         cudaStream_t s, unsigned long long* launches);
 cudaError_t launch_events(const DScene& sc, const StoreView& st, int32_t* pix, double* cos_le,
                           double* geom, double* ray_w, cudaStream_t s,
                           unsigned long long* launches);

@@ -107,6 +107,9 @@ def load_library(path: Optional[str] = None):
                                 C.POINTER(abi.ReconstructOpts), _dp, _u64p],
         "prc_gpu_last_timings": [vp, _dp],
         "prc_gpu_kernel_launches": [vp, _u64p],
+        "prc_gpu_timer_start": [vp],
+        "prc_gpu_timer_stop": [vp, _dp],
+        "prc_gpu_store_stats": [vp, vp, _u64p],
         "prc_gpu_debug_philox": [vp, C.c_uint64, C.c_uint64, C.c_uint64, _u32p],
         "prc_gpu_debug_walk": [vp, C.c_uint64, _dp, _u32p, _u32p, _dp, C.c_uint64],
         "prc_gpu_debug_pixel_of": [vp, C.c_int, C.c_uint64, _dp, _i32p],
@@ -387,6 +390,19 @@ class Context:
         _check(_lib.prc_gpu_last_timings(self.ptr, _ptr(ms, _dp)))
         return dict(zip(["prep", "forward", "image_allreduce", "gradient", "grad_allreduce_adam",
                          "total"], ms.tolist()))
+
+    def timer_start(self):
+        _check(_lib.prc_gpu_timer_start(self.ptr))
+
+    def timer_stop(self) -> float:
+        ms = C.c_double()
+        _check(_lib.prc_gpu_timer_stop(self.ptr, C.byref(ms)))
+        return ms.value
+
+    def store_stats(self, store: "PathStore") -> dict:
+        out = np.zeros(4, np.uint64)
+        _check(_lib.prc_gpu_store_stats(self.ptr, store.ptr, _ptr(out, _u64p)))
+        return dict(zip(["events", "live_path_spans", "le_spans", "path_spans"], out.tolist()))
 
     def kernel_launches(self) -> int:
         n = C.c_uint64()
