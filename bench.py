@@ -173,7 +173,8 @@ def run_ours(args):
                                          max_bounces=max_bounces(cfg)))
     t1 = time.time()
     store = rr.store
-    ctx.sort_by_size(store)
+    if not args.no_sort:
+        ctx.sort_by_size(store)
     t2 = time.time()
     info = store.info()
     stats = ctx.store_stats(store)  # global (allreduced)
@@ -257,6 +258,7 @@ def run_ours(args):
                        "events": int(E), "live_span_incidences": int(W_live),
                        "l2": "store >> L2 (126 MB), no flush needed",
                        "trace_s": round(t1 - t0, 3), "sort_s": round(t2 - t1, 3),
+                       "sorted_by_B": not args.no_sort,
                        "parallelism": f"paths sharded over {world} GPU(s), NCCL allreduce"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(),
@@ -342,6 +344,7 @@ def main():
     ap.add_argument("--cpu-paths", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-sort", action="store_true", help="evaluate the unsorted (path-major) store")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -104,6 +104,8 @@ struct prc_gpu_ctx {
     ncclComm_t comm = nullptr;
     cudaStream_t stream = nullptr;
     unsigned long long launches = 0;
+    int mode = 0;        // 0: event-major wavefront (default), 1: fused thread-per-path
+    int hash_bits = 12;  // K5b shared-memory hash: 2^hash_bits entries
     // scene
     bool have_scene = false;
     DScene dsc{};
@@ -168,8 +170,13 @@ struct prc_gpu_store {
     DBuf<int32_t> vox;
     DBuf<uint32_t> meta;
     unsigned long long n_rec = 0, n_iv = 0;
-    DBuf<float> ev_val;
+    DBuf<float> ev_val;    // event cache: [det][iv] (path mode) or [det][vt] (wavefront)
     DBuf<int32_t> ev_pix;
+    DBuf<double> lp, own;  // per interaction vertex: log-prefix (K4a), weight sum (K5b)
+    bool vt_ready = false; // Morton-ordered vertex table (wavefront mapping)
+    DBuf<double> vt_x, vt_y, vt_z, vt_dx, vt_dy, vt_dz;
+    DBuf<int32_t> vt_vox;
+    DBuf<uint32_t> vt_meta, vt_iv;
     DBuf<double> br_tot64;
     DBuf<float> sp_ref, br_tot;
     std::vector<double> ref_beta;
@@ -217,7 +224,8 @@ struct prc_gpu_store {
     unsigned long long device_bytes() const {
         return B.bytes() + stride.bytes() + stream.bytes() + rec_base.bytes() + iv_base.bytes() +
                trunc.bytes() + px.bytes() * 8 + vox.bytes() + meta.bytes() + ev_val.bytes() +
-               ev_pix.bytes() + br_tot64.bytes() + sp_ref.bytes() + br_tot.bytes();
+               ev_pix.bytes() + br_tot64.bytes() + sp_ref.bytes() + br_tot.bytes() + lp.bytes() +
+               own.bytes() + vt_x.bytes() * 6 + vt_vox.bytes() + vt_meta.bytes() + vt_iv.bytes();
     }
 };
 
@@ -436,25 +444,59 @@ struct EvalRun {
     const double* weights = nullptr;  // device
 };
 
-// Runs K3 prep, K4 forward (+ image allreduce) and optionally K5 (+ grad allreduce).
-// Leaves raw sums in c->images / c->g_span / c->g_vert / c->g_phong; returns clamps.
-unsigned long long run_eval(prc_gpu_ctx* c, prc_gpu_store* st, const Resolved& r, const EvalRun& er,
-                            const double* phong_dev) {
-    const DScene& s = c->dsc;
+// Vertex table of the event-major wavefront: interaction vertices in Morton order of
+// their position (built once per store layout; geometry only, so valid for any beta).
+void ensure_vertex_table(prc_gpu_ctx* c, prc_gpu_store* st) {
+    if (st->vt_ready) return;
+    const long long n = (long long)st->n_iv;
     cudaStream_t q = c->stream;
-    CK(cudaEventRecord(c->ev[0], q));
-    CK(launch_prep(s.n_species, c->V, r.src, st->br_tot64.p, c->sp_t.p, c->bt_tot.p, c->dbeta.p, q,
-                   &c->launches));
-    if (!phong_dev) {
-        const double ph[2] = {r.kappa, r.gamma};
-        CK(cudaMemcpyAsync(c->phong.p, ph, sizeof ph, cudaMemcpyHostToDevice, q));
-        phong_dev = c->phong.p;
+    const size_t nn = (size_t)std::max<long long>(n, 1);
+    st->vt_x.alloc(nn);
+    st->vt_y.alloc(nn);
+    st->vt_z.alloc(nn);
+    st->vt_dx.alloc(nn);
+    st->vt_dy.alloc(nn);
+    st->vt_dz.alloc(nn);
+    st->vt_vox.alloc(nn);
+    st->vt_meta.alloc(nn);
+    st->vt_iv.alloc(nn);
+    if (n > 0) {
+        DBuf<uint32_t> keys, keys_s, vals, vals_s;
+        DBuf<unsigned long long> iv_rec;
+        keys.alloc(nn);
+        keys_s.alloc(nn);
+        vals.alloc(nn);
+        vals_s.alloc(nn);
+        iv_rec.alloc(nn);
+        CK(launch_vt_keys(c->dsc, st->view(), keys.p, vals.p, iv_rec.p, q, &c->launches));
+        CK(sort_pairs_u32(keys.p, keys_s.p, vals.p, vals_s.p, n, &c->cub_tmp, &c->cub_bytes, q));
+        CK(launch_vt_gather(st->view(), vals_s.p, iv_rec.p, n, st->vt_x.p, st->vt_y.p, st->vt_z.p,
+                            st->vt_dx.p, st->vt_dy.p, st->vt_dz.p, st->vt_vox.p, st->vt_meta.p,
+                            st->vt_iv.p, q, &c->launches));
+        c->sync();
     }
-    const size_t slots = (size_t)s.n_det * (size_t)std::max<unsigned long long>(st->n_iv, 1);
-    st->ev_val.grow(slots);
-    st->ev_pix.grow(slots);
-    CK(cudaMemsetAsync(c->images.p, 0, c->images.bytes(), q));
-    CK(cudaMemsetAsync(c->clamps.p, 0, sizeof(unsigned long long), q));
+    st->vt_ready = true;
+}
+
+VertexTable vertex_table(prc_gpu_store* st) {
+    VertexTable v{};
+    v.n = st->n_iv;
+    v.x = st->vt_x.p;
+    v.y = st->vt_y.p;
+    v.z = st->vt_z.p;
+    v.dx = st->vt_dx.p;
+    v.dy = st->vt_dy.p;
+    v.dz = st->vt_dz.p;
+    v.vox = st->vt_vox.p;
+    v.meta = st->vt_meta.p;
+    v.iv = st->vt_iv.p;
+    v.ev_val = st->ev_val.p;
+    v.ev_pix = st->ev_pix.p;
+    return v;
+}
+
+EvalArgs eval_args(prc_gpu_ctx* c, prc_gpu_store* st, const EvalRun& er, const double* phong_dev) {
+    const DScene& s = c->dsc;
     EvalArgs ea{};
     ea.sp_t = c->sp_t.p;
     ea.sp_ref = st->sp_ref.p;
@@ -471,25 +513,75 @@ unsigned long long run_eval(prc_gpu_ctx* c, prc_gpu_store* st, const Resolved& r
     ea.per_species = er.per_species ? 1 : 0;
     ea.legacy = er.legacy ? 1 : 0;
     ea.do_beta = s.has_medium && (s.unknown >= 0 || er.per_species) ? 1 : 0;
-    StoreView sv = st->view();
+    return ea;
+}
+
+// K3 prep + K4 forward (+ image allreduce).  Raw pixel sums land in c->images.
+// Events [0]..[3] bracket prep / forward / allreduce.
+void run_forward(prc_gpu_ctx* c, prc_gpu_store* st, const Resolved& r, const EvalRun& er,
+                 const double*& phong_dev, EvalArgs& ea) {
+    const DScene& s = c->dsc;
+    cudaStream_t q = c->stream;
+    CK(cudaEventRecord(c->ev[0], q));
+    CK(launch_prep(s.n_species, c->V, r.src, st->br_tot64.p, c->sp_t.p, c->bt_tot.p, c->dbeta.p, q,
+                   &c->launches));
+    if (!phong_dev) {
+        const double ph[2] = {r.kappa, r.gamma};
+        CK(cudaMemcpyAsync(c->phong.p, ph, sizeof ph, cudaMemcpyHostToDevice, q));
+        phong_dev = c->phong.p;
+    }
+    const size_t slots = (size_t)s.n_det * (size_t)std::max<unsigned long long>(st->n_iv, 1);
+    st->ev_val.grow(slots);
+    st->ev_pix.grow(slots);
+    st->lp.grow((size_t)std::max<unsigned long long>(st->n_iv, 1));
+    st->own.grow((size_t)std::max<unsigned long long>(st->n_iv, 1));
+    if (c->mode == 0) ensure_vertex_table(c, st);
+    CK(cudaMemsetAsync(c->images.p, 0, c->images.bytes(), q));
+    CK(cudaMemsetAsync(c->clamps.p, 0, sizeof(unsigned long long), q));
+    ea = eval_args(c, st, er, phong_dev);
     CK(cudaEventRecord(c->ev[1], q));
-    CK(launch_forward(s, sv, ea, q, &c->launches));
+    if (c->mode == 0) {
+        CK(launch_prefix(s, st->view(), ea, st->lp.p, q, &c->launches));
+        CK(launch_le_forward(s, vertex_table(st), ea, st->lp.p, q, &c->launches));
+    } else {
+        CK(launch_forward(s, st->view(), ea, q, &c->launches));
+    }
     CK(cudaEventRecord(c->ev[2], q));
     c->allreduce(c->images.p, (size_t)c->n_pix);
     c->allreduce_u64(c->clamps.p, 1);
     CK(cudaEventRecord(c->ev[3], q));
-    if (er.want_grad) {
-        CK(cudaMemsetAsync(c->g_span.p, 0, c->g_span.bytes(), q));
-        CK(cudaMemsetAsync(c->g_vert.p, 0, c->g_vert.bytes(), q));
-        CK(cudaMemsetAsync(c->g_phong.p, 0, 2 * sizeof(double), q));
-        CK(launch_gradient(s, sv, ea, q, &c->launches));
+}
+
+// K5 gradient (+ gradient allreduce) with weights ea.weights.  Event [4] after K5.
+void run_gradient(prc_gpu_ctx* c, prc_gpu_store* st, const EvalArgs& ea) {
+    const DScene& s = c->dsc;
+    cudaStream_t q = c->stream;
+    CK(cudaMemsetAsync(c->g_span.p, 0, c->g_span.bytes(), q));
+    CK(cudaMemsetAsync(c->g_vert.p, 0, c->g_vert.bytes(), q));
+    CK(cudaMemsetAsync(c->g_phong.p, 0, 2 * sizeof(double), q));
+    if (c->mode == 0) {
+        CK(launch_le_gradient(s, vertex_table(st), ea, st->own.p, c->hash_bits, q, &c->launches));
+        CK(launch_path_gradient(s, st->view(), ea, st->own.p, q, &c->launches));
+    } else {
+        CK(launch_gradient(s, st->view(), ea, q, &c->launches));
     }
     CK(cudaEventRecord(c->ev[4], q));
-    if (er.want_grad) {
-        c->allreduce(c->g_span.p, c->g_span.n);
-        c->allreduce(c->g_vert.p, c->g_vert.n);
-        c->allreduce(c->g_phong.p, 2);
-    }
+    c->allreduce(c->g_span.p, c->g_span.n);
+    c->allreduce(c->g_vert.p, c->g_vert.n);
+    c->allreduce(c->g_phong.p, 2);
+}
+
+// Runs K3 prep, K4 forward (+ image allreduce) and optionally K5 (+ grad allreduce).
+// Leaves raw sums in c->images / c->g_span / c->g_vert / c->g_phong; returns clamps.
+unsigned long long run_eval(prc_gpu_ctx* c, prc_gpu_store* st, const Resolved& r, const EvalRun& er,
+                            const double* phong_dev) {
+    cudaStream_t q = c->stream;
+    EvalArgs ea;
+    run_forward(c, st, r, er, phong_dev, ea);
+    if (er.want_grad)
+        run_gradient(c, st, ea);
+    else
+        CK(cudaEventRecord(c->ev[4], q));
     unsigned long long cl = 0;
     CK(cudaMemcpyAsync(&cl, c->clamps.p, sizeof cl, cudaMemcpyDeviceToHost, q));
     return cl;
@@ -700,6 +792,7 @@ void sort_store(prc_gpu_ctx* c, prc_gpu_store* st) {
     st->vox.swap(ns->vox);
     st->meta.swap(ns->meta);
     st->sorted = true;
+    st->vt_ready = false;  // vertex table indexes the old layout
 }
 
 // ----------------------------------------------------------------------- PSTR I/O
@@ -1122,6 +1215,21 @@ PRC_EXPORT void prc_gpu_ctx_destroy(prc_gpu_ctx* ctx) {
     delete ctx;
 }
 
+PRC_EXPORT int prc_gpu_ctx_set_option(prc_gpu_ctx* ctx, const char* key, int64_t value) {
+    if (!ctx || !key) return fail(PRC_ERR_INVALID, "prc_gpu_ctx_set_option: null argument");
+    const std::string k(key);
+    if (k == "mode") {
+        if (value != 0 && value != 1) return fail(PRC_ERR_CONFIG, "mode must be 0 (wavefront) or 1 (path)");
+        ctx->mode = (int)value;
+    } else if (k == "hash_bits") {
+        if (value < 8 || value > 14) return fail(PRC_ERR_CONFIG, "hash_bits must be in 8..14");
+        ctx->hash_bits = (int)value;
+    } else {
+        return fail(PRC_ERR_CONFIG, "unknown option " + k);
+    }
+    return PRC_OK;
+}
+
 PRC_EXPORT int prc_gpu_ctx_rank(const prc_gpu_ctx* ctx, int* rank, int* world) {
     if (!ctx || !rank || !world) return fail(PRC_ERR_INVALID, "prc_gpu_ctx_rank: null argument");
     *rank = ctx->rank;
@@ -1378,38 +1486,15 @@ static double opt_step(prc_gpu_ctx* c, prc_gpu_store* st) {
         phong_dev = c->opt_x.p;
     }
     EvalRun er;
-    er.want_grad = false;
-    // K3 + K4 (+ image allreduce)
-    run_eval(c, st, r, er, phong_dev);
+    EvalArgs ea;
+    run_forward(c, st, r, er, phong_dev, ea);  // K3 + K4 (+ image allreduce)
     const double scale = 1.0 / (double)st->n_global;
     CK(launch_scale(c->images.p, c->n_pix, scale, q, &c->launches));
     CK(cudaMemsetAsync(c->loss.p, 0, 8, q));
     CK(launch_loss_residual(c->images.p, c->opt_gt.p, c->n_pix, c->weights.p, c->loss.p, q, &c->launches));
-    // K5 with residual weights (+ gradient allreduce)
-    StoreView sv = st->view();
-    EvalArgs ea{};
-    ea.sp_t = c->sp_t.p;
-    ea.sp_ref = st->sp_ref.p;
-    ea.bt_tot = c->bt_tot.p;
-    ea.br_tot = st->br_tot.p;
-    ea.dbeta = c->dbeta.p;
-    ea.phong = phong_dev ? phong_dev : c->phong.p;
-    ea.images = c->images.p;
-    ea.clamps = c->clamps.p;
-    ea.weights = c->weights.p;
-    ea.g_span = c->g_span.p;
-    ea.g_vert = c->g_vert.p;
-    ea.g_phong = c->g_phong.p;
+    ea.weights = c->weights.p;  // K5 with residual weights (+ gradient allreduce)
     ea.do_beta = s.has_medium && s.unknown >= 0 ? 1 : 0;
-    CK(cudaEventRecord(c->ev[3], q));
-    CK(cudaMemsetAsync(c->g_span.p, 0, c->g_span.bytes(), q));
-    CK(cudaMemsetAsync(c->g_vert.p, 0, c->g_vert.bytes(), q));
-    CK(cudaMemsetAsync(c->g_phong.p, 0, 16, q));
-    CK(launch_gradient(s, sv, ea, q, &c->launches));
-    CK(cudaEventRecord(c->ev[4], q));
-    c->allreduce(c->g_span.p, c->g_span.n);
-    c->allreduce(c->g_vert.p, c->g_vert.n);
-    c->allreduce(c->g_phong.p, 2);
+    run_gradient(c, st, ea);
     ++c->opt_t;
     const double c1 = 1.0 - std::pow(c->adam.eta1, (double)c->opt_t);
     const double c2 = 1.0 - std::pow(c->adam.eta2, (double)c->opt_t);

@@ -1,0 +1,121 @@
+// prc_eval.cuh — device helpers shared by the per-path and the event-major kernels:
+// local-estimation geometry (add_events, transport.cpp:218-254), the scattering
+// numerators of eval_record (pathstore.cpp:84-105) and the gradient score terms.
+#pragma once
+#include "prc_kernels.cuh"
+
+namespace prc {
+
+__device__ __forceinline__ double scat_num(const DScene& sc, const float* sp, int vox, double c) {
+    double num = 0.0;  // scat_num_t, pathstore.cpp:84-88
+    for (int j = 0; j < sc.n_species; ++j)
+        num += sc.sp[j].albedo * (double)sp[(long long)j * sc.V + vox] * phase_eval(sc.sp[j], c);
+    return num;
+}
+__device__ __forceinline__ double ext_num(const DScene& sc, const float* sp, int vox, double c) {
+    double num = 0.0;  // ext_num_ref, pathstore.cpp:90-94
+    for (int j = 0; j < sc.n_species; ++j)
+        num += (double)sp[(long long)j * sc.V + vox] * phase_eval(sc.sp[j], c);
+    return num;
+}
+__device__ __forceinline__ double surf_brdf(const DScene& sc, const double* phong, int s, double c) {
+    const DSurf& f = sc.surf[s];
+    if (f.target) return brdf_eval(1, 0.0, phong[0], phong[1], c);
+    return brdf_eval(f.brdf_kind, f.albedo, f.kappa, f.gamma, c);
+}
+
+// Local-estimation connection geometry (add_events, transport.cpp:218-254): the
+// connection direction w, distance r, 1/r^2 (x departure cosine at surfaces), the
+// visibility test against the surfaces and the lobe cosine.  Recomputed bit-exactly
+// from the stored vertex and incoming direction, so events are never stored.
+__device__ __forceinline__ bool event_geometry(const DScene& sc, const DDet& D, V3 x, V3 din,
+                                               uint32_t kind, int surf, V3& w, double& r,
+                                               double& geom, double& cos_le) {
+    const V3 to_det = ld3(D.pos) - x;
+    r = norm3(to_det);
+    if (r <= 0.0) return false;
+    w = to_det * (1.0 / r);
+    geom = 1.0 / (r * r);
+    V3 dir_ref = din;
+    int own = -1;
+    if (kind == VK_SURFACE) {
+        V3 n = normal_at(sc.surf[surf], x);
+        if (dot3(n, din) > 0.0) n = n * -1.0;
+        const double c_out = dot3(n, w);
+        if (c_out <= 0.0) return false;
+        geom *= c_out;
+        dir_ref = din - n * (2.0 * dot3(din, n));
+        own = surf;
+    }
+    if (sc.n_surf > 0) {
+        double th;
+        if (intersect_surfaces(sc, x, w, PRC_SELF_HIT_EPS, r - PRC_SELF_HIT_EPS, own, th) >= 0)
+            return false;
+    }
+    cos_le = dot3(dir_ref, w);
+    return true;
+}
+
+struct Rec {
+    V3 x, d;
+    double t, ct;
+    int vox;
+    uint32_t meta;
+};
+__device__ __forceinline__ Rec load_rec(const StoreView& st, unsigned long long r) {
+    Rec o;
+    o.x = mk(st.px[r], st.py[r], st.pz[r]);
+    o.d = mk(st.dx[r], st.dy[r], st.dz[r]);
+    o.t = st.tt[r];
+    o.ct = st.ct[r];
+    o.vox = st.vox[r];
+    o.meta = st.meta[r];
+    return o;
+}
+
+// Longest-processing-time first: the store is sorted by ascending B, so thread ids are
+// mapped back to front and the longest paths are scheduled in the first wave.
+__device__ __forceinline__ long long path_index(unsigned long long n) {
+    const unsigned long long g = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+    return g < n ? (long long)(n - 1 - g) : -1;
+}
+
+
+
+__device__ __forceinline__ void vertex_scores(const DScene& sc, const EvalArgs& ea, int vox,
+                                              double c, double wgt) {
+    // score_term, pathstore.cpp:97-105 (per species j when per_species is set)
+    if (ea.legacy) {
+        const double bt = (double)ea.bt_tot[vox];
+        const double s = bt > 0.0 ? 1.0 / bt : 0.0;
+        if (s == 0.0) return;
+        const int n_out = ea.per_species ? sc.n_species : 1;
+        for (int j = 0; j < n_out; ++j) atomicAdd(ea.g_vert + (long long)j * sc.V + vox, wgt * s);
+        return;
+    }
+    const double num = scat_num(sc, ea.sp_t, vox, c);
+    if (!(num > 0.0)) return;
+    if (ea.per_species) {
+        for (int j = 0; j < sc.n_species; ++j)
+            atomicAdd(ea.g_vert + (long long)j * sc.V + vox,
+                      wgt * (sc.sp[j].albedo * phase_eval(sc.sp[j], c) / num));
+    } else {
+        const DSpecies& u = sc.sp[sc.unknown];
+        atomicAdd(ea.g_vert + vox, wgt * (u.albedo * phase_eval(u, c) / num));
+    }
+}
+
+__device__ __forceinline__ void phong_scores(const double* phong, double c, double wgt, double& gk,
+                                             double& gg) {  // brdf.hpp:21-30
+    const double kap = phong[0], gam = phong[1];
+    const double cc = clampd(c, 0.0, 1.0);
+    const double pw = pow(cc, gam);
+    const double fr = 1.0 - kap + kap * pw;
+    if (fr > 0.0) {
+        gk += wgt * (-1.0 + pw) / fr;
+        gg += wgt * (cc <= 0.0 ? 0.0 : kap * pw * log(cc)) / fr;
+    }
+}
+
+
+}  // namespace prc

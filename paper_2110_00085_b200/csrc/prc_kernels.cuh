@@ -26,6 +26,21 @@ struct StoreView {
     int32_t* ev_pix;  // [det][iv]: pixel, -1 when no event
 };
 
+// Interaction vertices (b = 1..B-1 of every path) in Morton order of their position:
+// the unit of the event-major wavefront.  A CTA takes a contiguous run of vertices and
+// walks the cameras one after another, so a warp's 32 local-estimation rays start within
+// a voxel or two of each other and run to the same camera (coherent DDA trip counts,
+// L1-resident beta gathers, overlapping voxel sets for the gradient scatter).
+struct VertexTable {
+    unsigned long long n;
+    const double *x, *y, *z, *dx, *dy, *dz;
+    const int32_t* vox;
+    const uint32_t* meta;
+    const uint32_t* iv;  // interaction-vertex slot (path-layout index) of entry i
+    float* ev_val;       // [det][i] cached event value (K4b -> K5b)
+    int32_t* ev_pix;     // [det][i] pixel, -1 when no event
+};
+
 struct RecordsOut {
     double *px, *py, *pz, *dx, *dy, *dz, *tt, *ct;
     int32_t* vox;
@@ -124,6 +139,34 @@ cudaError_t launch_gather_records(const StoreView& old_st, const uint32_t* perm,
                                   const unsigned long long* rec_base_new,
                                   const uint32_t* stride_new, const RecordsOut& out,
                                   cudaStream_t s, unsigned long long* launches);
+
+// ---- event-major wavefront (default mapping) -------------------------------------
+// Vertex-table construction: Morton keys + iv -> record map, CUB radix sort, gather.
+cudaError_t launch_vt_keys(const DScene& sc, const StoreView& st, uint32_t* keys,
+                           uint32_t* iv_values, unsigned long long* iv_rec, cudaStream_t s,
+                           unsigned long long* launches);
+cudaError_t sort_pairs_u32(const uint32_t* keys_in, uint32_t* keys_out, const uint32_t* vals_in,
+                           uint32_t* vals_out, long long n, void** tmp, size_t* tmp_bytes,
+                           cudaStream_t s);
+cudaError_t launch_vt_gather(const StoreView& st, const uint32_t* vt2iv,
+                             const unsigned long long* iv_rec, long long n, double* x, double* y,
+                             double* z, double* dx, double* dy, double* dz, int32_t* vox,
+                             uint32_t* meta, uint32_t* iv, cudaStream_t s,
+                             unsigned long long* launches);
+// K4a: per-path log-prefix at every interaction vertex (lp[iv], -inf when dead).
+cudaError_t launch_prefix(const DScene& sc, const StoreView& st, const EvalArgs& ea, double* lp,
+                          cudaStream_t s, unsigned long long* launches);
+// K4b: per-event LE forward over the vertex table.
+cudaError_t launch_le_forward(const DScene& sc, const VertexTable& vt, const EvalArgs& ea,
+                              const double* lp, cudaStream_t s, unsigned long long* launches);
+// K5b: per-event LE gradient scatter (shared-memory hash, 2^hash_bits entries) and the
+// per-vertex event-weight sums own[iv].
+cudaError_t launch_le_gradient(const DScene& sc, const VertexTable& vt, const EvalArgs& ea,
+                               double* own, int hash_bits, cudaStream_t s,
+                               unsigned long long* launches);
+// K5a: per-path suffix pass (segment spans, continuation scores) from own[iv].
+cudaError_t launch_path_gradient(const DScene& sc, const StoreView& st, const EvalArgs& ea,
+                                 const double* own, cudaStream_t s, unsigned long long* launches);
 
 // ---- diagnostics / export ----------------------------------------------------------
 cudaError_t launch_philox(unsigned long long seed, unsigned long long stream,

@@ -1,0 +1,497 @@
+// prc_wavefront.cu — event-major wavefront for the recycled iteration (default mapping).
+//
+// The reference evaluates one stored path at a time (eval_record, pathstore.cpp:115-239).
+// Per path, ~97% of the voxel visits are local-estimation (LE) connections from the
+// interaction vertices to the cameras.  On the B200 the iteration is split:
+//
+//   K4a k_prefix        thread per path, B-sorted store (Path Sorting): incoming-segment
+//                       log-prefix at every interaction vertex -> lp[iv]
+//   K4b k_le_forward    CTA per run of Morton-ordered interaction vertices, camera by
+//                       camera: LE transmittance, event value, image scatter, event cache
+//   K5b k_le_gradient   same mapping: w = value * residual, LE scatter -w*l into a
+//                       shared-memory hash (flushed once per camera), vertex score terms,
+//                       per-vertex weight sums own[iv]
+//   K5a k_path_gradient thread per path: suffix sums from own[iv] -> incoming-segment
+//                       spans and continuation score terms
+//
+// All voxel indexing goes through the bit-exact fp64 DDA of prc_device.cuh.
+#include <cub/device/device_radix_sort.cuh>
+
+#include "prc_eval.cuh"
+
+using namespace prc;
+
+namespace {
+
+constexpr int kWF = 256;  // vertices per CTA in the wavefront kernels
+constexpr int kTPB = 128;
+constexpr uint32_t kEmpty = 0xffffffffu;
+
+inline unsigned grid_for(long long n, int tpb) {
+    long long g = (n + tpb - 1) / tpb;
+    return (unsigned)(g < 1 ? 1 : g);
+}
+
+__device__ __forceinline__ uint32_t spread10(uint32_t x) {  // 10 bits -> every third bit
+    x &= 0x3ffu;
+    x = (x | (x << 16)) & 0x030000ffu;
+    x = (x | (x << 8)) & 0x0300f00fu;
+    x = (x | (x << 4)) & 0x030c30c3u;
+    x = (x | (x << 2)) & 0x09249249u;
+    return x;
+}
+
+__device__ __forceinline__ uint32_t morton_key(const DScene& sc, V3 p) {
+    const double q[3] = {(p.x - sc.bmin[0]) / (sc.bmax[0] - sc.bmin[0]),
+                         (p.y - sc.bmin[1]) / (sc.bmax[1] - sc.bmin[1]),
+                         (p.z - sc.bmin[2]) / (sc.bmax[2] - sc.bmin[2])};
+    uint32_t c[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        double f = q[a] * 1024.0;
+        f = f < 0.0 ? 0.0 : (f > 1023.0 ? 1023.0 : f);
+        c[a] = (uint32_t)f;
+    }
+    return spread10(c[0]) | (spread10(c[1]) << 1) | (spread10(c[2]) << 2);
+}
+
+// ------------------------------------------------------------------ vertex table
+__global__ void k_vt_keys(const __grid_constant__ DScene sc, const __grid_constant__ StoreView st,
+                          uint32_t* keys, uint32_t* vals, unsigned long long* iv_rec) {
+    const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= (long long)st.n) return;
+    const int B = (int)st.B[p];
+    const unsigned long long rb = st.rec_base[p], ib = st.iv_base[p];
+    const unsigned rs = st.stride[p];
+    for (int b = 1; b < B; ++b) {
+        const unsigned long long r = rb + (unsigned long long)b * rs;
+        const unsigned long long iv = ib + (unsigned long long)(b - 1) * rs;
+        keys[iv] = morton_key(sc, mk(st.px[r], st.py[r], st.pz[r]));
+        vals[iv] = (uint32_t)iv;
+        iv_rec[iv] = r;
+    }
+}
+
+__global__ void k_vt_gather(const __grid_constant__ StoreView st, const uint32_t* vt2iv,
+                            const unsigned long long* iv_rec, long long n, double* x, double* y,
+                            double* z, double* dx, double* dy, double* dz, int32_t* vox,
+                            uint32_t* meta, uint32_t* iv) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t s = vt2iv[i];
+    const unsigned long long r = iv_rec[s];
+    x[i] = st.px[r];
+    y[i] = st.py[r];
+    z[i] = st.pz[r];
+    dx[i] = st.dx[r];
+    dy[i] = st.dy[r];
+    dz[i] = st.dz[r];
+    vox[i] = st.vox[r];
+    meta[i] = st.meta[r];
+    iv[i] = s;
+}
+
+// ------------------------------------------------------------------ K4a prefix
+__global__ void __launch_bounds__(kTPB) k_prefix(const __grid_constant__ DScene sc,
+                                                 const __grid_constant__ StoreView st,
+                                                 const __grid_constant__ EvalArgs ea, double* lp) {
+    const long long p = path_index(st.n);
+    if (p < 0) return;
+    const int B = (int)st.B[p];
+    if (B < 2) return;
+    const unsigned long long rb = st.rec_base[p], ib = st.iv_base[p];
+    const unsigned rs = st.stride[p];
+    V3 xprev = mk(st.px[rb], st.py[rb], st.pz[rb]);
+    double l = 0.0;
+    bool dead = false;
+    for (int b = 1; b < B; ++b) {
+        const unsigned long long r = rb + (unsigned long long)b * rs;
+        const unsigned long long iv = ib + (unsigned long long)(b - 1) * rs;
+        const V3 x = mk(st.px[r], st.py[r], st.pz[r]);
+        if (dead) {
+            lp[iv] = -INFINITY;
+            continue;
+        }
+        if (sc.has_medium) {
+            double diff = 0.0;
+            const float* db = ea.dbeta;
+            dda_walk(sc, xprev, mk(st.dx[r], st.dy[r], st.dz[r]), st.tt[r], [&](int v, double ta, double tb) {
+                diff = fma((double)__ldg(db + v), tb - ta, diff);
+                return true;
+            });
+            l -= diff;
+        }
+        lp[iv] = l;
+        const uint32_t m = st.meta[r];
+        const uint32_t kind = meta_kind(m);
+        const double ct = st.ct[r];
+        if (kind == VK_VOLUME) {  // continuation, pathstore.cpp:168-184
+            const int vox = st.vox[r];
+            const double num = scat_num(sc, ea.sp_t, vox, ct);
+            const double den = ext_num(sc, ea.sp_ref, vox, ct);
+            if (num <= 0.0 || den <= 0.0)
+                dead = true;
+            else
+                l += log(num) - log(den);
+        } else if (kind == VK_SURFACE) {
+            const double fr = surf_brdf(sc, ea.phong, meta_surface(m), ct);
+            if (fr <= 0.0)
+                dead = true;
+            else
+                l += log(PRC_PI * fr);
+        }
+        xprev = x;
+    }
+}
+
+// ------------------------------------------------------------------ K4b LE forward
+__global__ void __launch_bounds__(kWF, 3) k_le_forward(const __grid_constant__ DScene sc,
+                                                       const __grid_constant__ VertexTable vt,
+                                                       const __grid_constant__ EvalArgs ea,
+                                                       const double* __restrict__ lp) {
+    const unsigned long long i = (unsigned long long)blockIdx.x * kWF + threadIdx.x;
+    const bool act = i < vt.n;
+    V3 x = mk(0, 0, 0), d = mk(0, 0, 1);
+    int vox = 0;
+    uint32_t meta = 0;
+    double lpv = -INFINITY;
+    if (act) {
+        x = mk(vt.x[i], vt.y[i], vt.z[i]);
+        d = mk(vt.dx[i], vt.dy[i], vt.dz[i]);
+        vox = vt.vox[i];
+        meta = vt.meta[i];
+        lpv = lp[vt.iv[i]];
+    }
+    const uint32_t kind = meta_kind(meta);
+    const int surf = meta_surface(meta);
+    const bool live = act && lpv != -INFINITY;
+    const double den = (live && kind == VK_VOLUME) ? (double)ea.br_tot[vox] : 0.0;
+    unsigned clamps = 0;
+    for (int k = 0; k < sc.n_det; ++k) {
+        float val = 0.0f;
+        int pix = -1;
+        if (live) {
+            const DDet& D = sc.det[k];
+            pix = pixel_of(D, x);
+            V3 w;
+            double r, geom, cos_le;
+            if (pix >= 0 && event_geometry(sc, D, x, d, kind, surf, w, r, geom, cos_le)) {
+                double logval = -INFINITY;
+                if (kind == VK_VOLUME) {
+                    const double num = scat_num(sc, ea.sp_t, vox, cos_le);
+                    if (num > 0.0 && den > 0.0) logval = lpv + log(num) - log(den);
+                } else {
+                    const double fr = surf_brdf(sc, ea.phong, surf, cos_le);
+                    if (fr > 0.0) logval = lpv + log(fr);
+                }
+                if (logval != -INFINITY) {
+                    if (sc.has_medium) {
+                        double od = 0.0;
+                        const float* bt = ea.bt_tot;
+                        dda_walk(sc, x, w, r, [&](int v, double ta, double tb) {
+                            od = fma((double)__ldg(bt + v), tb - ta, od);
+                            return true;
+                        });
+                        logval -= od;
+                    }
+                    if (logval > PRC_LOG_CLAMP || logval < -PRC_LOG_CLAMP) {
+                        logval = clampd(logval, -PRC_LOG_CLAMP, PRC_LOG_CLAMP);
+                        ++clamps;
+                    }
+                    const double v = exp(logval) * geom * sc.prefactor;
+                    atomicAdd(ea.images + D.img_off + pix, v);
+                    val = (float)v;
+                }
+            } else {
+                pix = -1;
+            }
+        }
+        if (act) {
+            vt.ev_val[(unsigned long long)k * vt.n + i] = val;
+            vt.ev_pix[(unsigned long long)k * vt.n + i] = pix;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) clamps += __shfl_down_sync(0xffffffffu, clamps, o);
+    if ((threadIdx.x & 31) == 0 && clamps) atomicAdd(ea.clamps, (unsigned long long)clamps);
+}
+
+// ------------------------------------------------------------------ K5b LE gradient
+// Shared-memory open-addressing hash (voxel -> partial dL/dbeta, fp32) with linear
+// probing; overflow falls through to a direct global atomic.  Flushed with fp64 global
+// atomics once per camera, so a CTA's ~256 coherent rays hit L2 once per distinct voxel.
+struct SmemHash {
+    uint32_t* keys;
+    float* vals;
+    uint32_t mask;
+    int shift;
+    __device__ __forceinline__ void add(uint32_t v, float x, double* g) {
+        uint32_t h = (v * 2654435761u) >> shift;
+#pragma unroll 1
+        for (int probe = 0; probe < 8; ++probe) {
+            const uint32_t k = ((volatile uint32_t*)keys)[h];
+            if (k == v) {
+                atomicAdd(vals + h, x);
+                return;
+            }
+            if (k == kEmpty) {
+                const uint32_t old = atomicCAS(keys + h, kEmpty, v);
+                if (old == kEmpty || old == v) {
+                    atomicAdd(vals + h, x);
+                    return;
+                }
+            }
+            h = (h + 1) & mask;
+        }
+        atomicAdd(g + v, (double)x);
+    }
+};
+
+__device__ __forceinline__ double score_j(const DScene& sc, const EvalArgs& ea, int j, int vox,
+                                          double c, double num) {
+    // score_term, pathstore.cpp:97-105, for species j (legacy: 1 / beta_t_tot)
+    if (ea.legacy) {
+        const double bt = (double)ea.bt_tot[vox];
+        return bt > 0.0 ? 1.0 / bt : 0.0;
+    }
+    return num > 0.0 ? sc.sp[j].albedo * phase_eval(sc.sp[j], c) / num : 0.0;
+}
+
+constexpr int kMaxAcc = 4;
+
+__global__ void __launch_bounds__(kWF, 3) k_le_gradient(const __grid_constant__ DScene sc,
+                                                        const __grid_constant__ VertexTable vt,
+                                                        const __grid_constant__ EvalArgs ea,
+                                                        double* __restrict__ own, int hash_bits) {
+    extern __shared__ uint32_t smem[];
+    const int H = 1 << hash_bits;
+    SmemHash hs{smem, reinterpret_cast<float*>(smem + H), (uint32_t)(H - 1), 32 - hash_bits};
+    const bool use_hash = ea.do_beta && sc.has_medium;
+    if (use_hash)
+        for (int j = threadIdx.x; j < H; j += kWF) {
+            hs.keys[j] = kEmpty;
+            hs.vals[j] = 0.0f;
+        }
+    const unsigned long long i = (unsigned long long)blockIdx.x * kWF + threadIdx.x;
+    const bool act = i < vt.n;
+    V3 x = mk(0, 0, 0), d = mk(0, 0, 1);
+    int vox = 0;
+    uint32_t meta = 0;
+    if (act) {
+        x = mk(vt.x[i], vt.y[i], vt.z[i]);
+        d = mk(vt.dx[i], vt.dy[i], vt.dz[i]);
+        vox = vt.vox[i];
+        meta = vt.meta[i];
+    }
+    const uint32_t kind = meta_kind(meta);
+    const int surf = meta_surface(meta);
+    const bool on_target = sc.target >= 0 && kind == VK_SURFACE && surf == sc.target;
+    const int n_out = ea.per_species ? sc.n_species : 1;
+    double acc[kMaxAcc] = {0.0, 0.0, 0.0, 0.0};
+    double own_acc = 0.0, gk = 0.0, gg = 0.0;
+    if (use_hash) __syncthreads();
+    for (int k = 0; k < sc.n_det; ++k) {
+        double w = 0.0;
+        if (act) {
+            const int pix = vt.ev_pix[(unsigned long long)k * vt.n + i];
+            if (pix >= 0) {
+                const double val = (double)vt.ev_val[(unsigned long long)k * vt.n + i];
+                w = ea.weights ? val * ea.weights[sc.det[k].img_off + pix] : val;
+            }
+        }
+        if (w != 0.0) {
+            own_acc += w;
+            V3 wd;
+            double r, geom, cos_le;
+            event_geometry(sc, sc.det[k], x, d, kind, surf, wd, r, geom, cos_le);
+            if (use_hash) {
+                const float cf = (float)(-w);
+                double* g = ea.g_span;
+                dda_walk(sc, x, wd, r, [&](int v, double ta, double tb) {
+                    hs.add((uint32_t)v, cf * (float)(tb - ta), g);
+                    return true;
+                });
+            }
+            if (ea.do_beta && kind == VK_VOLUME) {
+                const double num = ea.legacy ? 0.0 : scat_num(sc, ea.sp_t, vox, cos_le);
+                if (ea.per_species) {
+                    for (int j = 0; j < sc.n_species; ++j) {
+                        const double s = w * score_j(sc, ea, j, vox, cos_le, num);
+                        if (j < kMaxAcc)
+                            acc[j] += s;
+                        else
+                            atomicAdd(ea.g_vert + (long long)j * sc.V + vox, s);
+                    }
+                } else {
+                    acc[0] += w * score_j(sc, ea, sc.unknown, vox, cos_le, num);
+                }
+            }
+            if (on_target) phong_scores(ea.phong, cos_le, w, gk, gg);
+        }
+        if (use_hash) {  // flush this camera's partial gradients
+            __syncthreads();
+            for (int j = threadIdx.x; j < H; j += kWF) {
+                const uint32_t key = hs.keys[j];
+                if (key != kEmpty) {
+                    atomicAdd(ea.g_span + key, (double)hs.vals[j]);
+                    hs.keys[j] = kEmpty;
+                    hs.vals[j] = 0.0f;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    if (act) {
+        own[vt.iv[i]] = own_acc;
+        if (ea.do_beta && kind == VK_VOLUME)
+            for (int j = 0; j < n_out && j < kMaxAcc; ++j)
+                if (acc[j] != 0.0) atomicAdd(ea.g_vert + (long long)j * sc.V + vox, acc[j]);
+    }
+    if (sc.target >= 0) {
+        for (int o = 16; o > 0; o >>= 1) {
+            gk += __shfl_down_sync(0xffffffffu, gk, o);
+            gg += __shfl_down_sync(0xffffffffu, gg, o);
+        }
+        if ((threadIdx.x & 31) == 0 && (gk != 0.0 || gg != 0.0)) {
+            atomicAdd(ea.g_phong, gk);
+            atomicAdd(ea.g_phong + 1, gg);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ K5a path suffix
+__global__ void __launch_bounds__(kTPB) k_path_gradient(const __grid_constant__ DScene sc,
+                                                        const __grid_constant__ StoreView st,
+                                                        const __grid_constant__ EvalArgs ea,
+                                                        const double* __restrict__ own) {
+    const long long p = path_index(st.n);
+    double gk = 0.0, gg = 0.0;
+    if (p >= 0) {
+        const int B = (int)st.B[p];
+        if (B >= 2) {
+            const unsigned long long rb = st.rec_base[p], ib = st.iv_base[p];
+            const unsigned rs = st.stride[p];
+            double W = 0.0;
+            bool any = false;
+            for (int b = 1; b < B; ++b) {
+                const double o = own[ib + (unsigned long long)(b - 1) * rs];
+                W += o;
+                any |= o != 0.0;
+            }
+            if (any) {
+                V3 xprev = mk(st.px[rb], st.py[rb], st.pz[rb]);
+                double prefix = 0.0;
+                for (int b = 1; b < B; ++b) {
+                    const unsigned long long r = rb + (unsigned long long)b * rs;
+                    const double o = own[ib + (unsigned long long)(b - 1) * rs];
+                    const double from_here = W - prefix;  // suffix sums of pathstore.cpp:219-237
+                    const double prefix_next = prefix + o;
+                    const double after = W - prefix_next;
+                    const V3 x = mk(st.px[r], st.py[r], st.pz[r]);
+                    if (from_here != 0.0 && ea.do_beta) {
+                        const double cf = -from_here;
+                        double* g = ea.g_span;
+                        dda_walk(sc, xprev, mk(st.dx[r], st.dy[r], st.dz[r]), st.tt[r],
+                                 [&](int v, double ta, double tb) {
+                                     atomicAdd(g + v, cf * (tb - ta));
+                                     return true;
+                                 });
+                    }
+                    if (after != 0.0) {
+                        const uint32_t m = st.meta[r];
+                        const uint32_t kind = meta_kind(m);
+                        if (kind == VK_VOLUME && ea.do_beta) vertex_scores(sc, ea, st.vox[r], st.ct[r], after);
+                        if (sc.target >= 0 && kind == VK_SURFACE && meta_surface(m) == sc.target)
+                            phong_scores(ea.phong, st.ct[r], after, gk, gg);
+                    }
+                    prefix = prefix_next;
+                    xprev = x;
+                }
+            }
+        }
+    }
+    if (sc.target >= 0) {
+        for (int o = 16; o > 0; o >>= 1) {
+            gk += __shfl_down_sync(0xffffffffu, gk, o);
+            gg += __shfl_down_sync(0xffffffffu, gg, o);
+        }
+        if ((threadIdx.x & 31) == 0 && (gk != 0.0 || gg != 0.0)) {
+            atomicAdd(ea.g_phong, gk);
+            atomicAdd(ea.g_phong + 1, gg);
+        }
+    }
+}
+
+}  // namespace
+
+#define LAUNCH_DONE()              \
+    do {                           \
+        if (launches) ++*launches; \
+        return cudaGetLastError(); \
+    } while (0)
+
+cudaError_t launch_vt_keys(const DScene& sc, const StoreView& st, uint32_t* keys, uint32_t* vals,
+                           unsigned long long* iv_rec, cudaStream_t s, unsigned long long* launches) {
+    if (st.n == 0) return cudaSuccess;
+    k_vt_keys<<<grid_for((long long)st.n, kTPB), kTPB, 0, s>>>(sc, st, keys, vals, iv_rec);
+    LAUNCH_DONE();
+}
+
+cudaError_t sort_pairs_u32(const uint32_t* ki, uint32_t* ko, const uint32_t* vi, uint32_t* vo,
+                           long long n, void** tmp, size_t* tmp_bytes, cudaStream_t s) {
+    size_t need = 0;
+    cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, need, ki, ko, vi, vo, (int64_t)n, 0, 30, s);
+    if (e != cudaSuccess) return e;
+    if (need > *tmp_bytes) {
+        if (*tmp) cudaFree(*tmp);
+        e = cudaMalloc(tmp, need);
+        if (e != cudaSuccess) {
+            *tmp = nullptr;
+            *tmp_bytes = 0;
+            return e;
+        }
+        *tmp_bytes = need;
+    }
+    return cub::DeviceRadixSort::SortPairs(*tmp, need, ki, ko, vi, vo, (int64_t)n, 0, 30, s);
+}
+
+cudaError_t launch_vt_gather(const StoreView& st, const uint32_t* vt2iv, const unsigned long long* iv_rec,
+                             long long n, double* x, double* y, double* z, double* dx, double* dy,
+                             double* dz, int32_t* vox, uint32_t* meta, uint32_t* iv, cudaStream_t s,
+                             unsigned long long* launches) {
+    if (n == 0) return cudaSuccess;
+    k_vt_gather<<<grid_for(n, 256), 256, 0, s>>>(st, vt2iv, iv_rec, n, x, y, z, dx, dy, dz, vox, meta, iv);
+    LAUNCH_DONE();
+}
+
+cudaError_t launch_prefix(const DScene& sc, const StoreView& st, const EvalArgs& ea, double* lp,
+                          cudaStream_t s, unsigned long long* launches) {
+    if (st.n == 0) return cudaSuccess;
+    k_prefix<<<grid_for((long long)st.n, kTPB), kTPB, 0, s>>>(sc, st, ea, lp);
+    LAUNCH_DONE();
+}
+
+cudaError_t launch_le_forward(const DScene& sc, const VertexTable& vt, const EvalArgs& ea,
+                              const double* lp, cudaStream_t s, unsigned long long* launches) {
+    if (vt.n == 0) return cudaSuccess;
+    k_le_forward<<<grid_for((long long)vt.n, kWF), kWF, 0, s>>>(sc, vt, ea, lp);
+    LAUNCH_DONE();
+}
+
+cudaError_t launch_le_gradient(const DScene& sc, const VertexTable& vt, const EvalArgs& ea, double* own,
+                               int hash_bits, cudaStream_t s, unsigned long long* launches) {
+    if (vt.n == 0) return cudaSuccess;
+    const size_t smem = (size_t)(1u << hash_bits) * 8u;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(k_le_gradient, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    k_le_gradient<<<grid_for((long long)vt.n, kWF), kWF, smem, s>>>(sc, vt, ea, own, hash_bits);
+    LAUNCH_DONE();
+}
+
+cudaError_t launch_path_gradient(const DScene& sc, const StoreView& st, const EvalArgs& ea,
+                                 const double* own, cudaStream_t s, unsigned long long* launches) {
+    if (st.n == 0) return cudaSuccess;
+    k_path_gradient<<<grid_for((long long)st.n, kTPB), kTPB, 0, s>>>(sc, st, ea, own);
+    LAUNCH_DONE();
+}

@@ -86,6 +86,7 @@ def load_library(path: Optional[str] = None):
         "prc_gpu_ctx_create_rank": [C.c_int, C.c_int, C.c_int, vp, C.POINTER(vp)],
         "prc_gpu_ctx_destroy": [vp],
         "prc_gpu_ctx_rank": [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)],
+        "prc_gpu_ctx_set_option": [vp, C.c_char_p, C.c_int64],
         "prc_gpu_scene_upload": [vp, vp],
         "prc_gpu_scene_voxel_count": [vp, _u64p],
         "prc_gpu_scene_pixel_count": [vp, _u64p],
@@ -266,6 +267,11 @@ class Context:
             self.close()
         except Exception:
             pass
+
+    def set_option(self, key: str, value: int):
+        """'mode': 0 event-major wavefront (default) / 1 fused thread-per-path;
+        'hash_bits': gradient shared-memory hash size (2^bits entries)."""
+        _check(_lib.prc_gpu_ctx_set_option(self.ptr, key.encode(), int(value)))
 
     # ------------------------------------------------------------------ scene
     def upload(self, scene: Scene):

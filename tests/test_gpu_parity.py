@@ -118,9 +118,16 @@ def test_sort_empty_store_rejected(ctx):
 
 
 # ---------------------------------------------------------------- K4/K5 on identical stores
+@pytest.fixture(params=[0, 1], ids=["wavefront", "per_path"])
+def mode(ctx, request):
+    ctx.set_option("mode", request.param)
+    yield request.param
+    ctx.set_option("mode", 0)
+
+
 @pytest.mark.parametrize("name", list(FIXTURES))
 @pytest.mark.parametrize("sort", [False, True])
-def test_evaluate_matches_reference_on_its_store(ctx, golden_dir, name, sort):
+def test_evaluate_matches_reference_on_its_store(ctx, golden_dir, name, sort, mode):
     scene = FIXTURES[name]["scene"]()
     g = golden(name)
     ctx.upload(scene)
@@ -145,10 +152,10 @@ def test_evaluate_matches_reference_on_its_store(ctx, golden_dir, name, sort):
         if scene.unknown_species() >= 0:
             r = ctx.evaluate_store(scene, st, params, EvalOptions(want_grad=True, legacy_score=True))
             assert grad_err(r.grad_beta, g[f"{tag}_legacy_grad"]) <= GRAD_TOL
-    print(f"{name} sort={sort}: max image rel err {worst[0]:.2e}, max grad rel err {worst[1]:.2e}")
+    print(f"{name} sort={sort} mode={mode}: max image rel err {worst[0]:.2e}, max grad rel err {worst[1]:.2e}")
 
 
-def test_per_type_gradients(ctx, golden_dir):
+def test_per_type_gradients(ctx, golden_dir, mode):
     """Config (c): both species' gradients from one pass; each equals the reference's
     single-unknown gradient with that species flagged (SURVEY a15 flip oracle)."""
     scene = FIXTURES["tomo2"]["scene"]()
@@ -188,7 +195,7 @@ def test_pstr_errors(ctx, tmp_path):
 
 # ---------------------------------------------------------------- K1 trace
 @pytest.mark.parametrize("name", list(FIXTURES))
-def test_device_store_round_trip_through_reference_format(ctx, port, tmp_path, name):
+def test_device_store_round_trip_through_reference_format(ctx, port, tmp_path, name, mode):
     """GPU-traced store -> PSTR (spans/events materialised on the device) -> oracle
     evaluates the identical stored path set; GPU evaluation agrees within 1e-5."""
     fx = FIXTURES[name]
