@@ -167,6 +167,16 @@ def run_ours(args):
     cfg = args.config
     scene = make_scene(cfg)
     n_paths = int(args.paths or CONFIGS[cfg]["paths"])
+    if args.mode is not None:
+        ctx.set_option("mode", args.mode)
+    if args.hash_bits is not None:
+        ctx.set_option("hash_bits", args.hash_bits)
+    if args.agg is not None:
+        ctx.set_option("agg", args.agg)
+    if args.spread is not None:
+        ctx.set_option("spread", args.spread)
+    if args.packet is not None:
+        ctx.set_option("packet", args.packet)
     ctx.upload(scene)
     t0 = time.time()
     rr = ctx.render(scene, RenderOptions(n_paths=n_paths, seed=7, keep_paths=True,
@@ -259,6 +269,8 @@ def run_ours(args):
                        "l2": "store >> L2 (126 MB), no flush needed",
                        "trace_s": round(t1 - t0, 3), "sort_s": round(t2 - t1, 3),
                        "sorted_by_B": not args.no_sort,
+                       "mode": "per_path" if args.mode == 1 else "wavefront",
+                       "hash_bits": args.hash_bits, "agg": args.agg, "spread": args.spread, "packet": args.packet,
                        "parallelism": f"paths sharded over {world} GPU(s), NCCL allreduce"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(),
@@ -345,6 +357,11 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sort", action="store_true", help="evaluate the unsorted (path-major) store")
+    ap.add_argument("--mode", type=int, default=None, help="0 wavefront (default), 1 fused per-path")
+    ap.add_argument("--hash-bits", type=int, default=None, help="K5b smem hash bits (0 = direct atomics)")
+    ap.add_argument("--agg", type=int, default=None, help="warp-aggregated reductions (0 off, 1 match, 2 runs)")
+    ap.add_argument("--spread", type=int, default=None, help="K5b lane spreading factor")
+    ap.add_argument("--packet", type=int, default=None, help="K5b rays per thread in lockstep")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

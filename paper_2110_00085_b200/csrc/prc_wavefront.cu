@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(kTPB) k_prefix(const __grid_constant__ DScene 
 __global__ void __launch_bounds__(kWF, 3) k_le_forward(const __grid_constant__ DScene sc,
                                                        const __grid_constant__ VertexTable vt,
                                                        const __grid_constant__ EvalArgs ea,
-                                                       const double* __restrict__ lp) {
+                                                       const double* __restrict__ lp, int agg) {
     const unsigned long long i = (unsigned long long)blockIdx.x * kWF + threadIdx.x;
     const bool act = i < vt.n;
     V3 x = mk(0, 0, 0), d = mk(0, 0, 1);
@@ -170,6 +170,7 @@ __global__ void __launch_bounds__(kWF, 3) k_le_forward(const __grid_constant__ D
     for (int k = 0; k < sc.n_det; ++k) {
         float val = 0.0f;
         int pix = -1;
+        double contrib = 0.0;
         if (live) {
             const DDet& D = sc.det[k];
             pix = pixel_of(D, x);
@@ -198,13 +199,23 @@ __global__ void __launch_bounds__(kWF, 3) k_le_forward(const __grid_constant__ D
                         logval = clampd(logval, -PRC_LOG_CLAMP, PRC_LOG_CLAMP);
                         ++clamps;
                     }
-                    const double v = exp(logval) * geom * sc.prefactor;
-                    atomicAdd(ea.images + D.img_off + pix, v);
-                    val = (float)v;
+                    contrib = exp(logval) * geom * sc.prefactor;
+                    val = (float)contrib;
                 }
             } else {
                 pix = -1;
             }
+        }
+        if (agg) {  // image scatter, aggregated over lanes landing in the same pixel
+            const WarpScale ws = warp_scale(contrib);
+            if (contrib != 0.0) {
+                if (agg == 1)
+                    agg_red(ea.images + sc.det[k].img_off, (unsigned)pix, contrib, ws);
+                else
+                    run_red(ea.images + sc.det[k].img_off, (unsigned)pix, contrib, ws);
+            }
+        } else if (contrib != 0.0) {
+            atomicAdd(ea.images + sc.det[k].img_off + pix, contrib);
         }
         if (act) {
             vt.ev_val[(unsigned long long)k * vt.n + i] = val;
@@ -261,17 +272,28 @@ constexpr int kMaxAcc = 4;
 __global__ void __launch_bounds__(kWF, 3) k_le_gradient(const __grid_constant__ DScene sc,
                                                         const __grid_constant__ VertexTable vt,
                                                         const __grid_constant__ EvalArgs ea,
-                                                        double* __restrict__ own, int hash_bits) {
+                                                        double* __restrict__ own, int hash_bits, int agg,
+                                                        int spread) {
     extern __shared__ uint32_t smem[];
     const int H = 1 << hash_bits;
     SmemHash hs{smem, reinterpret_cast<float*>(smem + H), (uint32_t)(H - 1), 32 - hash_bits};
-    const bool use_hash = ea.do_beta && sc.has_medium;
+    const bool use_hash = ea.do_beta && sc.has_medium && hash_bits > 0;
+    const bool direct = ea.do_beta && sc.has_medium && hash_bits == 0;
     if (use_hash)
         for (int j = threadIdx.x; j < H; j += kWF) {
             hs.keys[j] = kEmpty;
             hs.vals[j] = 0.0f;
         }
-    const unsigned long long i = (unsigned long long)blockIdx.x * kWF + threadIdx.x;
+    // Lane spreading: within each chunk of 32*spread vertices, lane l of warp w takes
+    // vertex l*spread + w, so one RED instruction touches 32 distinct Morton
+    // neighbourhoods instead of (at high vertex density) one voxel 32 times.
+    const unsigned long long g = (unsigned long long)blockIdx.x * kWF + threadIdx.x;
+    unsigned long long i = g;
+    if (spread > 1) {
+        const unsigned long long chunk = 32ull * (unsigned long long)spread;
+        const unsigned long long c0 = (g / chunk) * chunk;
+        if (c0 + chunk <= vt.n) i = c0 + (g % 32ull) * spread + ((g / 32ull) % spread);
+    }
     const bool act = i < vt.n;
     V3 x = mk(0, 0, 0), d = mk(0, 0, 1);
     int vox = 0;
@@ -286,6 +308,7 @@ __global__ void __launch_bounds__(kWF, 3) k_le_gradient(const __grid_constant__ 
     const int surf = meta_surface(meta);
     const bool on_target = sc.target >= 0 && kind == VK_SURFACE && surf == sc.target;
     const int n_out = ea.per_species ? sc.n_species : 1;
+    const double diag = 1.0000001 * sqrt(sc.vs[0] * sc.vs[0] + sc.vs[1] * sc.vs[1] + sc.vs[2] * sc.vs[2]);
     double acc[kMaxAcc] = {0.0, 0.0, 0.0, 0.0};
     double own_acc = 0.0, gk = 0.0, gg = 0.0;
     if (use_hash) __syncthreads();
@@ -298,6 +321,8 @@ __global__ void __launch_bounds__(kWF, 3) k_le_gradient(const __grid_constant__ 
                 w = ea.weights ? val * ea.weights[sc.det[k].img_off + pix] : val;
             }
         }
+        // warp-uniform fixed-point scale: |w * span| <= |w| * voxel diagonal
+        const WarpScale ws = warp_scale(fabs(w) * diag);
         if (w != 0.0) {
             own_acc += w;
             V3 wd;
@@ -308,6 +333,27 @@ __global__ void __launch_bounds__(kWF, 3) k_le_gradient(const __grid_constant__ 
                 double* g = ea.g_span;
                 dda_walk(sc, x, wd, r, [&](int v, double ta, double tb) {
                     hs.add((uint32_t)v, cf * (float)(tb - ta), g);
+                    return true;
+                });
+            } else if (direct && agg == 1) {  // warp-aggregated (MATCH) fp64 L2 reductions
+                const double cf = -w;
+                double* g = ea.g_span;
+                dda_walk(sc, x, wd, r, [&](int v, double ta, double tb) {
+                    agg_red(g, (unsigned)v, cf * (tb - ta), ws);
+                    return true;
+                });
+            } else if (direct && agg == 2) {  // adjacent-lane run aggregation
+                const double cf = -w;
+                double* g = ea.g_span;
+                dda_walk(sc, x, wd, r, [&](int v, double ta, double tb) {
+                    run_red(g, (unsigned)v, cf * (tb - ta), ws);
+                    return true;
+                });
+            } else if (direct) {  // one fp64 L2 reduction per voxel visit
+                const double cf = -w;
+                double* g = ea.g_span;
+                dda_walk(sc, x, wd, r, [&](int v, double ta, double tb) {
+                    atomicAdd(g + v, cf * (tb - ta));
                     return true;
                 });
             }
@@ -345,6 +391,124 @@ __global__ void __launch_bounds__(kWF, 3) k_le_gradient(const __grid_constant__ 
         if (ea.do_beta && kind == VK_VOLUME)
             for (int j = 0; j < n_out && j < kMaxAcc; ++j)
                 if (acc[j] != 0.0) atomicAdd(ea.g_vert + (long long)j * sc.V + vox, acc[j]);
+    }
+    if (sc.target >= 0) {
+        for (int o = 16; o > 0; o >>= 1) {
+            gk += __shfl_down_sync(0xffffffffu, gk, o);
+            gg += __shfl_down_sync(0xffffffffu, gg, o);
+        }
+        if ((threadIdx.x & 31) == 0 && (gk != 0.0 || gg != 0.0)) {
+            atomicAdd(ea.g_phong, gk);
+            atomicAdd(ea.g_phong + 1, gg);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ K5b, lockstep packets
+// One thread walks the LE rays of M consecutive Morton-ordered vertices (a packet: at
+// high vertex density they share a voxel) to the same camera in lockstep, one DDA step
+// per ray per iteration.  Spans that land in the same voxel at the same iteration are
+// summed in registers before a single fp64 L2 reduction, so the number of REDs falls
+// (~0.35 per voxel visit for M = 4 at 1e8 paths), while `spread` keeps the 32 lanes of a
+// warp on distinct packets far apart in Morton order (no same-address RED conflicts).
+template <int M>
+__global__ void __launch_bounds__(128, M == 2 ? 4 : 1) k_le_gradient_ms(const __grid_constant__ DScene sc,
+                                                        const __grid_constant__ VertexTable vt,
+                                                        const __grid_constant__ EvalArgs ea,
+                                                        double* __restrict__ own, int spread) {
+    const unsigned long long n_pk = (vt.n + M - 1) / M;
+    const unsigned long long g = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long pk = g;
+    if (spread > 1) {
+        const unsigned long long chunk = 32ull * (unsigned long long)spread;
+        const unsigned long long c0 = (g / chunk) * chunk;
+        if (c0 + chunk <= n_pk) pk = c0 + (g % 32ull) * spread + ((g / 32ull) % spread);
+    }
+    const bool single = !ea.per_species;
+    double own_acc[M], acc[M];
+#pragma unroll
+    for (int r = 0; r < M; ++r) own_acc[r] = acc[r] = 0.0;
+    double gk = 0.0, gg = 0.0;
+    for (int k = 0; k < sc.n_det; ++k) {
+        DdaState S[M];
+        double cf[M];
+#pragma unroll
+        for (int r = 0; r < M; ++r) {
+            S[r].alive = false;
+            cf[r] = 0.0;
+            const unsigned long long i = pk * M + r;
+            if (pk >= n_pk || i >= vt.n) continue;
+            const int pix = vt.ev_pix[(unsigned long long)k * vt.n + i];
+            if (pix < 0) continue;
+            const double val = (double)vt.ev_val[(unsigned long long)k * vt.n + i];
+            const double w = ea.weights ? val * ea.weights[sc.det[k].img_off + pix] : val;
+            if (w == 0.0) continue;
+            own_acc[r] += w;
+            const V3 x = mk(vt.x[i], vt.y[i], vt.z[i]);
+            const V3 d = mk(vt.dx[i], vt.dy[i], vt.dz[i]);
+            const uint32_t meta = vt.meta[i];
+            const uint32_t kind = meta_kind(meta);
+            const int surf = meta_surface(meta);
+            V3 wd;
+            double rr, geom, cos_le;
+            event_geometry(sc, sc.det[k], x, d, kind, surf, wd, rr, geom, cos_le);
+            if (ea.do_beta) {
+                S[r].init(sc, x, wd, rr);
+                cf[r] = -w;
+                if (kind == VK_VOLUME) {
+                    const int vox = vt.vox[i];
+                    const double num = ea.legacy ? 0.0 : scat_num(sc, ea.sp_t, vox, cos_le);
+                    if (single) {
+                        acc[r] += w * score_j(sc, ea, sc.unknown, vox, cos_le, num);
+                    } else {
+                        for (int j = 0; j < sc.n_species; ++j)
+                            atomicAdd(ea.g_vert + (long long)j * sc.V + vox,
+                                      w * score_j(sc, ea, j, vox, cos_le, num));
+                    }
+                }
+            }
+            if (sc.target >= 0 && kind == VK_SURFACE && surf == sc.target)
+                phong_scores(ea.phong, cos_le, w, gk, gg);
+        }
+        bool any = false;
+#pragma unroll
+        for (int r = 0; r < M; ++r) any |= S[r].alive;
+        while (any) {
+            int v[M];
+            double val[M];
+            bool e[M];
+#pragma unroll
+            for (int r = 0; r < M; ++r) {
+                double ta = 0.0, tb = 0.0;
+                e[r] = S[r].alive && S[r].step(sc, v[r], ta, tb);
+                val[r] = e[r] ? cf[r] * (tb - ta) : 0.0;
+            }
+#pragma unroll
+            for (int r = 1; r < M; ++r) {  // merge equal voxels into the first occurrence
+                bool merged = false;
+#pragma unroll
+                for (int q = 0; q < r; ++q) {
+                    if (!merged && e[r] && e[q] && v[q] == v[r]) {
+                        val[q] += val[r];
+                        merged = true;
+                    }
+                }
+                if (merged) e[r] = false;
+            }
+            any = false;
+#pragma unroll
+            for (int r = 0; r < M; ++r) {
+                if (e[r]) atomicAdd(ea.g_span + v[r], val[r]);
+                any |= S[r].alive;
+            }
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < M; ++r) {
+        const unsigned long long i = pk * M + r;
+        if (pk >= n_pk || i >= vt.n) continue;
+        own[vt.iv[i]] = own_acc[r];
+        if (single && acc[r] != 0.0) atomicAdd(ea.g_vert + vt.vox[i], acc[r]);
     }
     if (sc.target >= 0) {
         for (int o = 16; o > 0; o >>= 1) {
@@ -471,21 +635,32 @@ cudaError_t launch_prefix(const DScene& sc, const StoreView& st, const EvalArgs&
 }
 
 cudaError_t launch_le_forward(const DScene& sc, const VertexTable& vt, const EvalArgs& ea,
-                              const double* lp, cudaStream_t s, unsigned long long* launches) {
+                              const double* lp, int agg, cudaStream_t s, unsigned long long* launches) {
     if (vt.n == 0) return cudaSuccess;
-    k_le_forward<<<grid_for((long long)vt.n, kWF), kWF, 0, s>>>(sc, vt, ea, lp);
+    k_le_forward<<<grid_for((long long)vt.n, kWF), kWF, 0, s>>>(sc, vt, ea, lp, agg);
     LAUNCH_DONE();
 }
 
 cudaError_t launch_le_gradient(const DScene& sc, const VertexTable& vt, const EvalArgs& ea, double* own,
-                               int hash_bits, cudaStream_t s, unsigned long long* launches) {
+                               int hash_bits, int agg, int spread, int packet, cudaStream_t s,
+                               unsigned long long* launches) {
     if (vt.n == 0) return cudaSuccess;
-    const size_t smem = (size_t)(1u << hash_bits) * 8u;
+    if (packet > 1 && hash_bits == 0 && agg == 0) {
+        const long long n_pk = ((long long)vt.n + packet - 1) / packet;
+        if (packet == 2)
+            k_le_gradient_ms<2><<<grid_for(n_pk, 128), 128, 0, s>>>(sc, vt, ea, own, spread);
+        else if (packet == 4)
+            k_le_gradient_ms<4><<<grid_for(n_pk, 128), 128, 0, s>>>(sc, vt, ea, own, spread);
+        else
+            k_le_gradient_ms<8><<<grid_for(n_pk, 128), 128, 0, s>>>(sc, vt, ea, own, spread);
+        LAUNCH_DONE();
+    }
+    const size_t smem = hash_bits > 0 ? (size_t)(1u << hash_bits) * 8u : 0;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k_le_gradient, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
-    k_le_gradient<<<grid_for((long long)vt.n, kWF), kWF, smem, s>>>(sc, vt, ea, own, hash_bits);
+    k_le_gradient<<<grid_for((long long)vt.n, kWF), kWF, smem, s>>>(sc, vt, ea, own, hash_bits, agg, spread);
     LAUNCH_DONE();
 }
 

@@ -118,11 +118,18 @@ def test_sort_empty_store_rejected(ctx):
 
 
 # ---------------------------------------------------------------- K4/K5 on identical stores
-@pytest.fixture(params=[0, 1], ids=["wavefront", "per_path"])
+MAPPINGS = {"wavefront": dict(mode=0, packet=1), "wavefront_p2": dict(mode=0, packet=2),
+            "wavefront_p4": dict(mode=0, packet=4), "per_path": dict(mode=1, packet=1)}
+
+
+@pytest.fixture(params=list(MAPPINGS))
 def mode(ctx, request):
-    ctx.set_option("mode", request.param)
+    """Every kernel mapping must meet the same parity bar."""
+    for k, v in MAPPINGS[request.param].items():
+        ctx.set_option(k, v)
     yield request.param
     ctx.set_option("mode", 0)
+    ctx.set_option("packet", 2)
 
 
 @pytest.mark.parametrize("name", list(FIXTURES))
