@@ -106,7 +106,7 @@ struct prc_gpu_ctx {
     unsigned long long launches = 0;
     int mode = 0;        // 0: event-major wavefront (default), 1: fused thread-per-path
     int hash_bits = 0;   // K5b: 0 = direct fp64 L2 reductions (measured fastest); else smem hash 2^bits
-    int spread = 32;     // K5b lane spreading factor (measured: 8 best at 1e7, 64 at 1e8)
+    int spread = 64;     // K5b lane spreading factor (packet 2: 8 best at 1e7, 64-128 at 1e8)
     int packet = 2;      // K5b rays per thread walked in lockstep (measured best: 2)
     int agg = 0;         // warp-aggregated reductions (match + fixed-point REDUX): measured slower, off
     // scene
@@ -134,6 +134,12 @@ struct prc_gpu_ctx {
     int64_t opt_t = 0;
     prc_gpu_adam_config adam{};
     int n_step_scale = 0;
+    // forward-reuse cache: grad_forward right after recycled_render at the same point
+    // (inverse.cpp:205, 246) reuses the stored forward instead of recomputing K3/K4
+    unsigned long long fwd_gen = 0;
+    unsigned long long last_fwd_gen = ~0ull, last_fwd_key = 0;
+    const prc_gpu_store* last_fwd_store = nullptr;
+    unsigned long long last_fwd_clamps = 0;
     // timing
     cudaEvent_t ev[6] = {};
     cudaEvent_t timer[2] = {};
@@ -441,6 +447,38 @@ Resolved resolve_params(prc_gpu_ctx* c, const prc_gpu_params* p, const prc_gpu_s
     return r;
 }
 
+// 64-bit content hash of the evaluated parameters (forward-reuse key).
+unsigned long long mix64(unsigned long long h, unsigned long long x) {
+    h ^= x + 0x9E3779B97F4A7C15ull + (h << 6) + (h >> 2);
+    return h * 0xff51afd7ed558ccdull;
+}
+unsigned long long hash_doubles(unsigned long long h, const double* p, size_t n) {
+    const unsigned long long* w = reinterpret_cast<const unsigned long long*>(p);
+    unsigned long long a = h, b = h ^ 0x632be59bd9b4e019ull;
+    size_t i = 0;
+    for (; i + 1 < n; i += 2) {
+        a = (a ^ w[i]) * 0x9E3779B97F4A7C15ull;
+        b = (b ^ w[i + 1]) * 0xC2B2AE3D27D4EB4Full;
+    }
+    if (i < n) a = (a ^ w[i]) * 0x9E3779B97F4A7C15ull;
+    return mix64(a, b);
+}
+unsigned long long params_key(const prc_gpu_ctx* c, const prc_gpu_params* p, const prc_gpu_store* st,
+                              int flags) {
+    unsigned long long h = mix64(0x1234567ull, (unsigned long long)(uintptr_t)st);
+    h = mix64(h, (unsigned long long)c->mode);
+    h = mix64(h, (unsigned long long)(flags & PRC_EVAL_NORMALIZE));
+    if (!p) return mix64(h, 0xabcdefull);
+    double kg[2] = {p->kappa_s, p->gamma};
+    h = hash_doubles(h, kg, 2);
+    if (p->beta) h = hash_doubles(mix64(h, p->n_beta), p->beta, (size_t)p->n_beta);
+    if (p->species_beta)
+        for (int j = 0; j < c->dsc.n_species; ++j)
+            h = p->species_beta[j] ? hash_doubles(mix64(h, 100 + j), p->species_beta[j], (size_t)c->V)
+                                   : mix64(h, 200 + j);
+    return h;
+}
+
 // ----------------------------------------------------------------------- K3 + K4 + K5
 struct EvalRun {
     bool want_grad = false, per_species = false, legacy = false, normalize = true;
@@ -538,6 +576,7 @@ void run_forward(prc_gpu_ctx* c, prc_gpu_store* st, const Resolved& r, const Eva
     st->ev_pix.grow(slots);
     st->lp.grow((size_t)std::max<unsigned long long>(st->n_iv, 1));
     st->own.grow((size_t)std::max<unsigned long long>(st->n_iv, 1));
+    ++c->fwd_gen;  // invalidates any cached forward
     if (c->mode == 0) ensure_vertex_table(c, st);
     CK(cudaMemsetAsync(c->images.p, 0, c->images.bytes(), q));
     CK(cudaMemsetAsync(c->clamps.p, 0, sizeof(unsigned long long), q));
@@ -797,6 +836,7 @@ void sort_store(prc_gpu_ctx* c, prc_gpu_store* st) {
     st->meta.swap(ns->meta);
     st->sorted = true;
     st->vt_ready = false;  // vertex table indexes the old layout
+    ++c->fwd_gen;          // the event cache indexes the old layout too
 }
 
 // ----------------------------------------------------------------------- PSTR I/O
@@ -1372,6 +1412,7 @@ PRC_EXPORT int prc_gpu_store_import_pstr(prc_gpu_ctx* ctx, const char* path, prc
     begin(ctx);
     ctx->check_scene();
     *out = import_pstr(ctx, path).release();
+    ++ctx->fwd_gen;
     ABI_CATCH
 }
 
@@ -1384,6 +1425,7 @@ PRC_EXPORT int prc_gpu_store_set_generation(prc_gpu_store* st, uint64_t g) {
 PRC_EXPORT void prc_gpu_store_free(prc_gpu_store* st) {
     if (!st) return;
     cudaSetDevice(st->ctx->device);
+    ++st->ctx->fwd_gen;  // a later store may reuse this address
     delete st;
 }
 
@@ -1398,19 +1440,34 @@ PRC_EXPORT int prc_gpu_evaluate(prc_gpu_ctx* ctx, const prc_gpu_store* store,
     begin(ctx);
     ctx->check_scene();
     auto* st = const_cast<prc_gpu_store*>(store);
-    Resolved r = resolve_params(ctx, params, st);
     EvalRun er;
     er.want_grad = (flags & PRC_EVAL_WANT_GRAD) != 0;
     er.per_species = (flags & PRC_EVAL_PER_SPECIES) != 0;
     er.legacy = (flags & PRC_EVAL_LEGACY_SCORE) != 0;
+    const double scale = (flags & PRC_EVAL_NORMALIZE) && st->n_global ? 1.0 / (double)st->n_global : 1.0;
+    const unsigned long long key = params_key(ctx, params, st, flags);
+    const bool reuse = er.want_grad && ctx->last_fwd_store == st && ctx->last_fwd_gen == ctx->fwd_gen &&
+                       ctx->last_fwd_key == key;
     if (er.want_grad && opts && opts->pixel_weights) {
         CK(cudaMemcpyAsync(ctx->weights.p, opts->pixel_weights, (size_t)ctx->n_pix * 8,
                            cudaMemcpyHostToDevice, ctx->stream));
         er.weights = ctx->weights.p;
     }
-    const unsigned long long cl = run_eval(ctx, st, r, er, nullptr);
-    const double scale = (flags & PRC_EVAL_NORMALIZE) && st->n_global ? 1.0 / (double)st->n_global : 1.0;
-    CK(launch_scale(ctx->images.p, ctx->n_pix, scale, ctx->stream, &ctx->launches));
+    unsigned long long cl;
+    if (reuse) {  // images, event cache, prep fields and Phong values are still current
+        cudaStream_t q = ctx->stream;
+        for (int i = 0; i < 4; ++i) CK(cudaEventRecord(ctx->ev[i], q));
+        EvalArgs ea = eval_args(ctx, st, er, ctx->phong.p);
+        run_gradient(ctx, st, ea);
+        cl = ctx->last_fwd_clamps;
+    } else {
+        Resolved r = resolve_params(ctx, params, st);
+        cl = run_eval(ctx, st, r, er, nullptr);
+        CK(launch_scale(ctx->images.p, ctx->n_pix, scale, ctx->stream, &ctx->launches));
+        ctx->last_fwd_store = st;
+        ctx->last_fwd_gen = ctx->fwd_gen;
+        ctx->last_fwd_key = key;
+    }
     copy_out(ctx, res->images, ctx->images.p, (size_t)ctx->n_pix);
     const DScene& s = ctx->dsc;
     res->grad_kappa = res->grad_gamma = 0.0;
@@ -1431,6 +1488,7 @@ PRC_EXPORT int prc_gpu_evaluate(prc_gpu_ctx* ctx, const prc_gpu_store* store,
         CK(cudaEventRecord(ctx->ev[5], ctx->stream));
         record_timings(ctx);
     }
+    ctx->last_fwd_clamps = cl;
     res->clamp_events = cl;
     res->mean_correction = 1.0;
     ABI_CATCH

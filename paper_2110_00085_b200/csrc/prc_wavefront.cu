@@ -470,36 +470,52 @@ __global__ void __launch_bounds__(128, M == 2 ? 4 : 1) k_le_gradient_ms(const __
             if (sc.target >= 0 && kind == VK_SURFACE && surf == sc.target)
                 phong_scores(ea.phong, cos_le, w, gk, gg);
         }
-        bool any = false;
-#pragma unroll
-        for (int r = 0; r < M; ++r) any |= S[r].alive;
-        while (any) {
-            int v[M];
-            double val[M];
-            bool e[M];
-#pragma unroll
-            for (int r = 0; r < M; ++r) {
-                double ta = 0.0, tb = 0.0;
-                e[r] = S[r].alive && S[r].step(sc, v[r], ta, tb);
-                val[r] = e[r] ? cf[r] * (tb - ta) : 0.0;
-            }
-#pragma unroll
-            for (int r = 1; r < M; ++r) {  // merge equal voxels into the first occurrence
-                bool merged = false;
-#pragma unroll
-                for (int q = 0; q < r; ++q) {
-                    if (!merged && e[r] && e[q] && v[q] == v[r]) {
-                        val[q] += val[r];
-                        merged = true;
-                    }
+        const int nx = sc.dims[0], ny = sc.dims[1], nz = sc.dims[2];
+        double* g = ea.g_span;
+        if (M == 2) {  // hand-scheduled pair
+            while (S[0].alive || S[1].alive) {
+                double l0 = 0.0, l1 = 0.0;
+                const int v0 = S[0].alive ? dda_step_len(S[0], nx, ny, nz, l0) : -1;
+                const int v1 = S[1].alive ? dda_step_len(S[1], nx, ny, nz, l1) : -1;
+                const double x0 = cf[0] * l0, x1 = cf[1] * l1;
+                if (v0 >= 0 && v0 == v1) {
+                    atomicAdd(g + v0, x0 + x1);
+                } else {
+                    if (v0 >= 0) atomicAdd(g + v0, x0);
+                    if (v1 >= 0) atomicAdd(g + v1, x1);
                 }
-                if (merged) e[r] = false;
             }
-            any = false;
+        } else {
+            bool any = false;
 #pragma unroll
-            for (int r = 0; r < M; ++r) {
-                if (e[r]) atomicAdd(ea.g_span + v[r], val[r]);
-                any |= S[r].alive;
+            for (int r = 0; r < M; ++r) any |= S[r].alive;
+            while (any) {
+                int v[M];
+                double val[M];
+#pragma unroll
+                for (int r = 0; r < M; ++r) {
+                    double l = 0.0;
+                    v[r] = S[r].alive ? dda_step_len(S[r], nx, ny, nz, l) : -1;
+                    val[r] = cf[r] * l;
+                }
+#pragma unroll
+                for (int r = 1; r < M; ++r) {  // merge equal voxels into the first occurrence
+                    bool merged = false;
+#pragma unroll
+                    for (int q = 0; q < r; ++q) {
+                        if (!merged && v[r] >= 0 && v[q] == v[r]) {
+                            val[q] += val[r];
+                            merged = true;
+                        }
+                    }
+                    if (merged) v[r] = -1;
+                }
+                any = false;
+#pragma unroll
+                for (int r = 0; r < M; ++r) {
+                    if (v[r] >= 0) atomicAdd(g + v[r], val[r]);
+                    any |= S[r].alive;
+                }
             }
         }
     }

@@ -335,3 +335,31 @@ def test_phong_reconstruct_moves_toward_truth(ctx):
     p = out["params"]
     assert abs(p.kappa_s - 0.7) < abs(0.4 - 0.7) and abs(p.gamma - 50.0) < abs(25.0 - 50.0)
     assert out["loss"][-1] < out["loss"][0]
+
+
+def test_grad_forward_reuses_forward_cache_correctly(ctx, golden_dir):
+    """recycled_render then grad_forward at the same point reuses the cached forward;
+    any change of parameters, store layout or store invalidates it."""
+    scene = FIXTURES["tomo2"]["scene"]()
+    g = golden("tomo2")
+    ctx.upload(scene)
+    st = ctx.load_store(str(golden_dir / "tomo2.pstr"))
+    w = weight_patterns(scene)["w"]
+    p = perturbed(scene)
+    f = ctx.evaluate_store(scene, st, p, EvalOptions())
+    n0 = ctx.kernel_launches()
+    r = ctx.evaluate_store(scene, st, p, EvalOptions(want_grad=True, pixel_weights=w))
+    reused_launches = ctx.kernel_launches() - n0
+    assert grad_err(r.grad_beta, g["pert_w_grad"]) <= GRAD_TOL
+    assert np.array_equal(r.images, f.images)
+    # different parameters: no reuse, still correct
+    r2 = ctx.evaluate_store(scene, st, None, EvalOptions(want_grad=True, pixel_weights=w))
+    assert grad_err(r2.grad_beta, g["ref_w_grad"]) <= GRAD_TOL
+    n0 = ctx.kernel_launches()
+    ctx.evaluate_store(scene, st, p, EvalOptions(want_grad=True, pixel_weights=w))
+    assert ctx.kernel_launches() - n0 > reused_launches
+    # sort invalidates
+    ctx.evaluate_store(scene, st, p, EvalOptions())
+    ctx.sort_by_size(st)
+    r3 = ctx.evaluate_store(scene, st, p, EvalOptions(want_grad=True, pixel_weights=w))
+    assert grad_err(r3.grad_beta, g["pert_w_grad"]) <= GRAD_TOL
