@@ -292,11 +292,12 @@ def cpu_baseline(cfg, scene, n_cpu=None):
         ref, kind = None, "port"
     tp = t_params(scene)
     if ref is not None:
-        st = ref.time_iteration(scene, None, tp, n, 7, cores, reps=1)
+        st = ref.time_iteration(scene, None, tp, n, 7, cores, reps=3, warmup=1)
         secs = st["forward_s"] + st["grad_s"]
         return {"value": st["segments"] / secs, "unit": "path-segments/s", "cores": cores,
                 "kind": kind, "sample": f"{n} paths of the same workload, traced then sorted; "
-                f"timed recycled_render + grad_forward ({secs:.2f} s, {cores} threads)",
+                f"mean of 3 timed recycled_render + grad_forward iterations after 1 warm-up "
+                f"({secs:.2f} s each, {cores} threads)",
                 "forward_s": st["forward_s"], "grad_s": st["grad_s"]}
     port = pyoracle.Port()
     _, _, store = port.render(scene, n, 7)
@@ -327,7 +328,8 @@ def run_reference(args):
         print(json.dumps({"impl": "reference", "unavailable": f"oracle/_ref not built: {e}"}))
         return
     tp = t_params(scene)
-    st = ref.time_iteration(scene, None, tp, n, 7, cores, reps=max(1, args.steps))
+    st = ref.time_iteration(scene, None, tp, n, 7, cores, reps=max(1, args.steps),
+                            warmup=max(0, args.warmup))
     secs = st["forward_s"] + st["grad_s"]
     value = st["segments"] / secs
     line = {"impl": "reference", "metric": "recycled path-segments/sec per render+gradient iteration",

@@ -1378,6 +1378,40 @@ int orc_load_pstr(const char* path, orc_store** out) { /* pathstore.cpp:460-516 
     return 0;
 }
 
+/* Contiguous shard [lo, hi) of the records (deep copy), for the multi-rank decomposition
+ * tests: rank r of W owns records [N r / W, N (r + 1) / W). */
+orc_store* orc_store_slice(const orc_store* s, uint64_t lo, uint64_t hi) {
+    orc_store* o = (orc_store*)calloc(1, sizeof *o);
+    o->n = hi > lo ? hi - lo : 0;
+    o->rec = (Rec*)calloc((size_t)(o->n ? o->n : 1), sizeof(Rec));
+    for (uint64_t i = 0; i < o->n; ++i) {
+        const Rec* a = &s->rec[lo + i];
+        Rec* b = &o->rec[i];
+        *b = *a;
+        b->v = (Vtx*)malloc((size_t)(a->nv ? a->nv : 1) * sizeof(Vtx));
+        memcpy(b->v, a->v, (size_t)a->nv * sizeof(Vtx));
+        b->cv = a->nv;
+        b->sp = (Span*)malloc((size_t)(a->ns ? a->ns : 1) * sizeof(Span));
+        memcpy(b->sp, a->sp, (size_t)a->ns * sizeof(Span));
+        b->cs = a->ns;
+        b->ev = (Evt*)malloc((size_t)(a->ne ? a->ne : 1) * sizeof(Evt));
+        memcpy(b->ev, a->ev, (size_t)a->ne * sizeof(Evt));
+        b->ce = a->ne;
+        b->le = (Span*)malloc((size_t)(a->nl ? a->nl : 1) * sizeof(Span));
+        memcpy(b->le, a->le, (size_t)a->nl * sizeof(Span));
+        b->cl = a->nl;
+    }
+    o->generation = s->generation;
+    o->seed = s->seed;
+    o->n_ref_beta = s->n_ref_beta;
+    o->ref_beta = (double*)malloc((size_t)(s->n_ref_beta ? s->n_ref_beta : 1) * sizeof(double));
+    memcpy(o->ref_beta, s->ref_beta, (size_t)s->n_ref_beta * sizeof(double));
+    o->ref_kappa = s->ref_kappa;
+    o->ref_gamma = s->ref_gamma;
+    rebuild_index(o);
+    return o;
+}
+
 uint64_t orc_store_count(const orc_store* s) { return s->n; }
 int orc_store_streams(const orc_store* s, uint64_t* out) {
     for (uint64_t i = 0; i < s->n; ++i) out[i] = s->rec[i].stream;

@@ -44,6 +44,8 @@ int orc_evaluate(const prc_scene_desc* d, const orc_store* s, const prc_gpu_para
 int orc_save_pstr(const orc_store* s, const char* path);
 int orc_load_pstr(const char* path, orc_store** out);
 uint64_t orc_store_count(const orc_store* s);
+/* Deep copy of records [lo, hi) (multi-rank decomposition tests). */
+orc_store* orc_store_slice(const orc_store* s, uint64_t lo, uint64_t hi);
 int orc_store_streams(const orc_store* s, uint64_t* out);
 int orc_store_sizes(const orc_store* s, uint32_t* out);
 /* Per-store statistics: [0] S, [1] vertices, [2] events, [3] LE spans,

@@ -79,6 +79,9 @@ class _Store:
                 "truncated"]
         return dict(zip(keys, o.tolist()))
 
+    def slice(self, lo: int, hi: int) -> "_Store":
+        return _Store(self.lib, self.lib.orc_store_slice(self.ptr, lo, hi))
+
     def sort_by_size(self):
         if self.lib.orc_sort_by_size(self.ptr):
             raise ValueError(self.lib.orc_last_error().decode())
@@ -97,9 +100,6 @@ class Port:
         L.orc_last_error.restype = C.c_char_p
         L.orc_store_count.restype = C.c_uint64
         L.orc_store_count.argtypes = [C.c_void_p]
-        for f in ("orc_store_streams", "orc_store_sizes", "orc_store_stats", "orc_sort_by_size",
-                  "orc_save_pstr", "orc_store_free"):
-            getattr(L, f).argtypes = None
         L.orc_store_free.argtypes = [C.c_void_p]
         L.orc_store_streams.argtypes = [C.c_void_p, _u64p]
         L.orc_store_sizes.argtypes = [C.c_void_p, _u32p]
@@ -112,6 +112,8 @@ class Port:
         L.orc_evaluate.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, _dp, _dp, _dp, _dp,
                                    _dp, _u64p, _dp]
         L.orc_philox.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, _u32p]
+        L.orc_store_slice.restype = C.c_void_p
+        L.orc_store_slice.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64]
         L.orc_walk.argtypes = [C.c_void_p, C.c_uint64, _dp, _u32p, _u32p, _dp, C.c_uint64]
         L.orc_pixel_of.argtypes = [C.c_void_p, C.c_int, C.c_uint64, _dp, _i32p]
 
@@ -198,7 +200,7 @@ class Reference:
         L.ref_evaluate.argtypes = [C.c_void_p, C.c_char_p, C.c_void_p, C.c_int, _dp, C.c_int, _dp,
                                    _dp, _dp, _dp, _u64p, _dp]
         L.ref_time_iteration.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64,
-                                         C.c_uint64, C.c_int, C.c_int, _dp]
+                                         C.c_uint64, C.c_int, C.c_int, C.c_int, _dp]
         L.ref_reconstruct.argtypes = [C.c_void_p, C.c_void_p, _dp, C.c_double, _dp, C.c_int,
                                       C.c_uint64, C.c_uint64, C.c_int, C.c_int, C.c_int, _dp, _dp,
                                       _dp, _dp, _u64p]
@@ -270,11 +272,11 @@ class Reference:
                     grad_gamma=gg.value, clamp_events=int(cl.value), mean_correction=mc.value)
 
     def time_iteration(self, scene: Scene, ref: Optional[ParamSet], t: ParamSet, n: int, seed: int,
-                       workers: int, reps: int = 1) -> dict:
+                       workers: int, reps: int = 1, warmup: int = 0) -> dict:
         h = scene.desc()
         pr, pt = ParamsHolder(ref), ParamsHolder(t)
         st = np.zeros(9)
-        if self.lib.ref_time_iteration(h.ptr, pr.ptr, pt.ptr, n, seed, workers, reps,
+        if self.lib.ref_time_iteration(h.ptr, pr.ptr, pt.ptr, n, seed, workers, warmup, reps,
                                        _ptr(st, _dp)):
             raise ValueError(self._err())
         keys = ["segments", "trace_s", "sort_s", "forward_s", "grad_s", "events", "le_spans",

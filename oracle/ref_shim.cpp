@@ -255,13 +255,13 @@ int ref_evaluate(const prc_scene_desc* d, const char* pstr, const prc_gpu_params
     }
 }
 
-/* CPU baseline: render(keep) + sort, then time `reps` recycled iterations
+/* CPU baseline: render(keep) + sort, then `warmup` untimed and `reps` timed recycled iterations
  * (recycled_render + residual + grad_forward) at params t with `workers` threads.
  * stats[0]=segments S, [1]=trace s, [2]=sort s, [3]=mean forward s, [4]=mean grad s,
  * [5]=events, [6]=live LE spans, [7]=live path spans, [8]=vertices. */
 int ref_time_iteration(const prc_scene_desc* d, const prc_gpu_params* ref_params,
                        const prc_gpu_params* t_params, uint64_t n, uint64_t seed, int workers,
-                       int reps, double* stats) {
+                       int warmup, int reps, double* stats) {
     try {
         Scene s = make_scene(d);
         bind(s, make_params(s, ref_params));
@@ -291,7 +291,7 @@ int ref_time_iteration(const prc_scene_desc* d, const prc_gpu_params* ref_params
         for (auto& im : gt)
             for (auto& px : im.data) px *= 0.9;
         double fwd = 0, grd = 0;
-        for (int k = 0; k < reps; ++k) {
+        for (int k = -warmup; k < reps; ++k) {
             double a = now();
             ImageSet f = recycled_render(s, st, t, workers);
             double b = now();
@@ -304,6 +304,7 @@ int ref_time_iteration(const prc_scene_desc* d, const prc_gpu_params* ref_params
             SparseGradient g = grad_forward(s, st, t, go);
             double c = now();
             (void)g;
+            if (k < 0) continue;  // untimed warm-up iterations
             fwd += b - a;
             grd += c - b;
         }

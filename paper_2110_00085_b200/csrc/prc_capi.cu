@@ -158,11 +158,11 @@ struct prc_gpu_ctx {
         if (!have_scene) throw Err(PRC_ERR_INVALID, "no scene uploaded");
     }
     void allreduce(double* buf, size_t count) {
-        if (world > 1 && count > 0)
+        if (comm && count > 0)
             NK(ncclAllReduce(buf, buf, count, ncclFloat64, ncclSum, comm, stream));
     }
     void allreduce_u64(unsigned long long* buf, size_t count) {
-        if (world > 1 && count > 0)
+        if (comm && count > 0)
             NK(ncclAllReduce(buf, buf, count, ncclUint64, ncclSum, comm, stream));
     }
 };
@@ -1244,7 +1244,7 @@ PRC_EXPORT int prc_gpu_ctx_create_rank(int device, int rank, int world, const vo
     ctx_init(c.get(), device);
     c->rank = rank;
     c->world = world;
-    if (world > 1) {
+    if (nccl_id) {  // world 1 with an id builds a 1-rank communicator (exercises NCCL)
         ncclUniqueId id;
         std::memcpy(&id, nccl_id, sizeof id);
         NK(ncclCommInitRank(&c->comm, world, id, rank));
@@ -1344,7 +1344,7 @@ PRC_EXPORT int prc_gpu_render(prc_gpu_ctx* ctx, const prc_gpu_render_opts* opts,
     ctx->sync();
     if (truncated_out) {
         double t = (double)st->truncated;
-        if (ctx->world > 1) {
+        if (ctx->comm) {
             CK(cudaMemcpy(ctx->loss.p, &t, 8, cudaMemcpyHostToDevice));
             ctx->allreduce(ctx->loss.p, 1);
             ctx->sync();

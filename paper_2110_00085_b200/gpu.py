@@ -241,7 +241,7 @@ class Context:
                  nccl_id: Optional[bytes] = None):
         load_library()
         p = C.c_void_p()
-        if world == 1:
+        if world == 1 and nccl_id is None:
             _check(_lib.prc_gpu_ctx_create(device, C.byref(p)))
         else:
             buf = C.create_string_buffer(bytes(nccl_id), 128)

@@ -1,0 +1,118 @@
+// C++ host-API test (run by tests/test_host_api.py on a B200).  Drives the engine only
+// through include/pathrec_gpu.hpp — the reference-shaped C++ API — and checks results
+// against the C restatement oracle (oracle/_build/liboracle.so, linked as the checker).
+#include <cmath>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "../../oracle/pathrec_oracle.h"
+#include "pathrec_gpu.hpp"
+
+using namespace pathrec_gpu;
+
+static Scene two_species_cube(int n) {  // tests/helpers.hpp:56-79
+    Scene s;
+    s.bounds_min = {0, 0, 0};
+    s.bounds_max = {1, 1, 1};
+    GridGeometry g;
+    g.dims[0] = g.dims[1] = g.dims[2] = n;
+    g.voxel_size = {1.0 / n, 1.0 / n, 1.0 / n};
+    ParticleSpecies cloud, air;
+    cloud.extinction.geom = air.extinction.geom = g;
+    for (int v = 0; v < n * n * n; ++v) {
+        cloud.extinction.values.push_back(2.0 + 0.5 * (v % 7));
+        air.extinction.values.push_back(0.04);
+    }
+    cloud.albedo = 0.99;
+    cloud.phase = PhaseFunction::henyey_greenstein(0.5);
+    cloud.unknown = true;
+    air.albedo = 0.912;
+    air.phase = PhaseFunction::rayleigh();
+    s.species = {cloud, air};
+    s.light.kind = LightSource::Kind::IsotropicPoint;
+    s.light.position = {0.5, 0.5, 0.5};
+    Detector d;
+    d.position = {0.5, 0.5, 3.0};
+    d.direction = {0, 0, -1};
+    d.up = {0, 1, 0};
+    d.rows = d.cols = 6;
+    d.fov = 0.6;
+    s.detectors = {d};
+    return s;
+}
+
+int main() {
+    Context ctx(0);
+    Scene s = two_species_cube(4);
+    RenderOptions ro;
+    ro.n_paths = 3000;
+    ro.seed = 13;
+    ro.keep_paths = true;
+    RenderResult rr = render(ctx, s, ro);
+    sort_by_size(*rr.store);
+    if (!rr.store->sorted_flag()) return 2;
+    ParamSet t = params_from_scene(s);
+    for (size_t v = 0; v < t.beta.size(); ++v) t.beta[v] *= 1.0 + 0.02 * (v % 7);
+    ImageSet w = rr.images;
+    for (auto& im : w)
+        for (size_t p = 0; p < im.data.size(); ++p) im.data[p] = 1.0 + (p % 5);
+    EvalOptions eo;
+    eo.pixel_weights = &w;
+    SparseGradient g = grad_forward(s, *rr.store, t, eo);
+    ImageSet img = recycled_render(s, *rr.store, t);
+    // oracle on the identical stored path set (PSTR written by the device)
+    save_store(*rr.store, "host_api_test.pstr");
+    orc_store* os = nullptr;
+    if (orc_load_pstr("host_api_test.pstr", &os)) return 3;
+    Context::Holder h(s);
+    prc_gpu_params pc{t.beta.data(), t.beta.size(), 0.0, 0.0, nullptr};
+    std::vector<double> oimg(36), ograd(64), wflat;
+    for (auto& im : w) wflat.insert(wflat.end(), im.data.begin(), im.data.end());
+    double gk, gg, mc;
+    uint64_t cl;
+    if (orc_evaluate(&h.desc, os, &pc, PRC_EVAL_NORMALIZE | PRC_EVAL_WANT_GRAD, wflat.data(), oimg.data(),
+                     ograd.data(), &gk, &gg, &cl, &mc))
+        return 4;
+    double imax = 0, gmax = 0, ei = 0, eg = 0;
+    for (double x : oimg) imax = std::fmax(imax, std::fabs(x));
+    for (double x : ograd) gmax = std::fmax(gmax, std::fabs(x));
+    for (size_t p = 0; p < 36; ++p)
+        ei = std::fmax(ei, std::fabs(img[0].data[p] - oimg[p]) / std::fmax(std::fabs(oimg[p]), 1e-3 * imax));
+    for (int v = 0; v < 64; ++v) eg = std::fmax(eg, std::fabs(g.at(v) - ograd[v]) / gmax);
+    orc_store_free(os);
+    std::printf("host api: image rel err %.3e grad rel err %.3e\n", ei, eg);
+    if (!(ei <= 1e-5 && eg <= 1e-5)) return 5;
+    // reference exception behaviour
+    bool threw = false;
+    try {
+        EvalOptions bad;
+        bad.self_normalize = true;
+        evaluate_store(s, *rr.store, t, bad);
+    } catch (const std::invalid_argument&) {
+        threw = true;
+    }
+    if (!threw) return 6;
+    threw = false;
+    try {
+        load_store(ctx, s, "no_such_file.pstr");
+    } catch (const std::runtime_error&) {
+        threw = true;
+    }
+    if (!threw) return 7;
+    // Algorithm 2 on the device
+    ImageSet gt = render(ctx, s, RenderOptions{20000, 99, 1, 500, -1, false}).images;
+    ReconstructOptions opt;
+    opt.adam.alpha = 0.05;
+    opt.recycle_period = 5;
+    opt.max_iterations = 12;
+    opt.n_paths = 5000;
+    ParamSet init;
+    init.beta.assign(64, 3.0);
+    ReconstructResult res = reconstruct(ctx, s, gt, init, opt);
+    std::printf("reconstruct: phases %llu loss %.3e -> %.3e\n", (unsigned long long)res.sampling_phases,
+                res.loss.front(), res.loss.back());
+    if (res.sampling_phases != 3 || !(res.loss.back() < res.loss.front())) return 8;
+    std::remove("host_api_test.pstr");
+    return 0;
+}

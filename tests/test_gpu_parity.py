@@ -363,3 +363,20 @@ def test_grad_forward_reuses_forward_cache_correctly(ctx, golden_dir):
     ctx.sort_by_size(st)
     r3 = ctx.evaluate_store(scene, st, p, EvalOptions(want_grad=True, pixel_weights=w))
     assert grad_err(r3.grad_beta, g["pert_w_grad"]) <= GRAD_TOL
+
+
+def test_nccl_communicator_path(golden_dir):
+    """A context built on an NCCL communicator (1 rank here: one GPU per gpurun box) runs
+    the allreduce code path of K4/K5 and returns the same results."""
+    from paper_2110_00085_b200.gpu import Context
+    c = Context(0, 0, 1, Context.nccl_unique_id())
+    scene = FIXTURES["tomo2"]["scene"]()
+    g = golden("tomo2")
+    c.upload(scene)
+    st = c.load_store(str(golden_dir / "tomo2.pstr"))
+    r = c.evaluate_store(scene, st, perturbed(scene),
+                         EvalOptions(want_grad=True, pixel_weights=weight_patterns(scene)["w"]))
+    assert img_err(r.images, g["pert_w_images"]) <= IMG_TOL
+    assert grad_err(r.grad_beta, g["pert_w_grad"]) <= GRAD_TOL
+    st.free()
+    c.close()
