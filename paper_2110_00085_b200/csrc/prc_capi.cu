@@ -294,6 +294,7 @@ void upload_scene(prc_gpu_ctx* c, const prc_scene_desc* d) {
         V = (long long)s.dims[0] * s.dims[1] * s.dims[2];
     }
     s.V = V;
+    s.dda_packed = s.has_medium && s.dims[0] <= 512 && s.dims[1] <= 512 && s.dims[2] <= 512 ? 1 : 0;
     s.unknown = -1;
     std::vector<double> sp((size_t)d->n_species * (size_t)V);
     for (int j = 0; j < d->n_species; ++j) {
@@ -602,7 +603,8 @@ void run_gradient(prc_gpu_ctx* c, prc_gpu_store* st, const EvalArgs& ea) {
     CK(cudaMemsetAsync(c->g_vert.p, 0, c->g_vert.bytes(), q));
     CK(cudaMemsetAsync(c->g_phong.p, 0, 2 * sizeof(double), q));
     if (c->mode == 0) {
-        CK(launch_le_gradient(s, vertex_table(st), ea, st->own.p, c->hash_bits, c->agg, c->spread, c->packet, q,
+        CK(launch_le_gradient(s, vertex_table(st), ea, st->own.p, c->hash_bits, c->agg, c->spread,
+                                  s.dda_packed ? c->packet : 1, q,
                               &c->launches));
         CK(launch_path_gradient(s, st->view(), ea, st->own.p, q, &c->launches));
     } else {

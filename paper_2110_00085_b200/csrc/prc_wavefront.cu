@@ -145,19 +145,19 @@ __global__ void __launch_bounds__(kTPB) k_prefix(const __grid_constant__ DScene 
 }
 
 // ------------------------------------------------------------------ K4b LE forward
-__global__ void __launch_bounds__(kWF, 3) k_le_forward(const __grid_constant__ DScene sc,
+#ifndef PRC_FWD_MINB
+#define PRC_FWD_MINB 4
+#endif
+__global__ void __launch_bounds__(kWF, PRC_FWD_MINB) k_le_forward(const __grid_constant__ DScene sc,
                                                        const __grid_constant__ VertexTable vt,
                                                        const __grid_constant__ EvalArgs ea,
                                                        const double* __restrict__ lp, int agg) {
     const unsigned long long i = (unsigned long long)blockIdx.x * kWF + threadIdx.x;
     const bool act = i < vt.n;
-    V3 x = mk(0, 0, 0), d = mk(0, 0, 1);
     int vox = 0;
     uint32_t meta = 0;
     double lpv = -INFINITY;
     if (act) {
-        x = mk(vt.x[i], vt.y[i], vt.z[i]);
-        d = mk(vt.dx[i], vt.dy[i], vt.dz[i]);
         vox = vt.vox[i];
         meta = vt.meta[i];
         lpv = lp[vt.iv[i]];
@@ -172,11 +172,15 @@ __global__ void __launch_bounds__(kWF, 3) k_le_forward(const __grid_constant__ D
         int pix = -1;
         double contrib = 0.0;
         if (live) {
+            // vertex position/direction re-read per camera (L1 hits) instead of being kept
+            // live across the DDA: frees registers for the walk's loop invariants
+            const V3 x = mk(vt.x[i], vt.y[i], vt.z[i]);
             const DDet& D = sc.det[k];
             pix = pixel_of(D, x);
             V3 w;
             double r, geom, cos_le;
-            if (pix >= 0 && event_geometry(sc, D, x, d, kind, surf, w, r, geom, cos_le)) {
+            if (pix >= 0 &&
+                event_geometry(sc, D, x, mk(vt.dx[i], vt.dy[i], vt.dz[i]), kind, surf, w, r, geom, cos_le)) {
                 double logval = -INFINITY;
                 if (kind == VK_VOLUME) {
                     const double num = scat_num(sc, ea.sp_t, vox, cos_le);
@@ -412,7 +416,10 @@ __global__ void __launch_bounds__(kWF, 3) k_le_gradient(const __grid_constant__ 
 // (~0.35 per voxel visit for M = 4 at 1e8 paths), while `spread` keeps the 32 lanes of a
 // warp on distinct packets far apart in Morton order (no same-address RED conflicts).
 template <int M>
-__global__ void __launch_bounds__(128, M == 2 ? 4 : 1) k_le_gradient_ms(const __grid_constant__ DScene sc,
+#ifndef PRC_GRAD_MINB
+#define PRC_GRAD_MINB 4
+#endif
+__global__ void __launch_bounds__(128, M == 2 ? PRC_GRAD_MINB : 1) k_le_gradient_ms(const __grid_constant__ DScene sc,
                                                         const __grid_constant__ VertexTable vt,
                                                         const __grid_constant__ EvalArgs ea,
                                                         double* __restrict__ own, int spread) {

@@ -68,7 +68,7 @@ def load_library(path: Optional[str] = None):
     global _lib
     if _lib is not None:
         return _lib
-    path = path or LIB_PATH
+    path = path or os.environ.get("PRC_LIB") or LIB_PATH  # PRC_LIB: A/B experiment builds
     if path == LIB_PATH:
         from .build import build  # in-tree build; the .so normally ships prebuilt
         try:
