@@ -166,7 +166,7 @@ cudaError_t launch_le_forward(const DScene& sc, const VertexTable& vt, const Eva
 // spread: lane-spreading factor of the K5b vertex assignment (1 = coherent warps).
 cudaError_t launch_le_gradient(const DScene& sc, const VertexTable& vt, const EvalArgs& ea,
                                double* own, int hash_bits, int agg, int spread, int packet,
-                               cudaStream_t s, unsigned long long* launches);
+                               int tree, cudaStream_t s, unsigned long long* launches);
 // K5a: per-path suffix pass (segment spans, continuation scores) from own[iv].
 cudaError_t launch_path_gradient(const DScene& sc, const StoreView& st, const EvalArgs& ea,
                                  const double* own, cudaStream_t s, unsigned long long* launches);

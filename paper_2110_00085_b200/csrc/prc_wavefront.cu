@@ -545,6 +545,110 @@ __global__ void __launch_bounds__(128, M == 2 ? PRC_GRAD_MINB : 1) k_le_gradient
     }
 }
 
+// ------------------------------------------------------------------ K5b, shuffle tree
+// One LE ray per thread on the lean single-ray walk.  Lanes come in groups of 4 that hold
+// consecutive Morton vertices (their rays to one camera advance through the same voxels
+// at the same iteration); groups are spread `spread` apart in Morton order.  At every
+// emitted span, `rounds` butterfly steps (lane^1, then lane^2) fold the partner's
+// contribution into the lower lane when both sit in the same voxel, so one REDG serves
+// the group.  Partners that are not emitting this iteration are not merged (exact).
+__device__ __forceinline__ void tree_red(double* g, int v, double x, int rounds) {
+    const unsigned act = __activemask();
+    const int lane = threadIdx.x & 31;
+    bool keep = true;
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        if (r >= rounds) break;
+        const int m = 1 << r;
+        const int pv = __shfl_xor_sync(act, keep ? v : -1, m);
+        const double px = __shfl_xor_sync(act, x, m);
+        const bool pact = (act >> (lane ^ m)) & 1u;
+        if (keep && pact && pv == v) {
+            if (lane & m)
+                keep = false;
+            else
+                x += px;
+        }
+    }
+    if (keep) atomicAdd(g + v, x);
+}
+
+__global__ void __launch_bounds__(kWF, PRC_FWD_MINB) k_le_gradient_tree(
+    const __grid_constant__ DScene sc, const __grid_constant__ VertexTable vt,
+    const __grid_constant__ EvalArgs ea, double* __restrict__ own, int spread, int rounds) {
+    // group-granular spreading: lane l of warp w -> group (l/4)*spread + w, member l%4
+    const unsigned long long g = (unsigned long long)blockIdx.x * kWF + threadIdx.x;
+    unsigned long long i = g;
+    if (spread > 1) {
+        const unsigned long long chunk = 32ull * (unsigned long long)spread;
+        const unsigned long long c0 = (g / chunk) * chunk;
+        if (c0 + chunk <= vt.n) {
+            const unsigned long long lane = g % 32ull, w = (g / 32ull) % spread;
+            i = c0 + (((lane >> 2) * spread + w) << 2) + (lane & 3ull);
+        }
+    }
+    const bool act = i < vt.n;
+    int vox = 0;
+    uint32_t meta = 0;
+    if (act) {
+        vox = vt.vox[i];
+        meta = vt.meta[i];
+    }
+    const uint32_t kind = meta_kind(meta);
+    const int surf = meta_surface(meta);
+    const bool on_target = sc.target >= 0 && kind == VK_SURFACE && surf == sc.target;
+    const bool single = !ea.per_species;
+    double own_acc = 0.0, acc = 0.0, gk = 0.0, gg = 0.0;
+    for (int k = 0; k < sc.n_det; ++k) {
+        double w = 0.0;
+        if (act) {
+            const int pix = vt.ev_pix[(unsigned long long)k * vt.n + i];
+            if (pix >= 0) {
+                const double val = (double)vt.ev_val[(unsigned long long)k * vt.n + i];
+                w = ea.weights ? val * ea.weights[sc.det[k].img_off + pix] : val;
+            }
+        }
+        if (w == 0.0) continue;
+        own_acc += w;
+        const V3 x = mk(vt.x[i], vt.y[i], vt.z[i]);
+        V3 wd;
+        double r, geom, cos_le;
+        event_geometry(sc, sc.det[k], x, mk(vt.dx[i], vt.dy[i], vt.dz[i]), kind, surf, wd, r, geom, cos_le);
+        if (ea.do_beta) {
+            const double cf = -w;
+            double* gs = ea.g_span;
+            dda_walk(sc, x, wd, r, [&](int v, double ta, double tb) {
+                tree_red(gs, v, cf * (tb - ta), rounds);
+                return true;
+            });
+            if (kind == VK_VOLUME) {
+                const double num = ea.legacy ? 0.0 : scat_num(sc, ea.sp_t, vox, cos_le);
+                if (single) {
+                    acc += w * score_j(sc, ea, sc.unknown, vox, cos_le, num);
+                } else {
+                    for (int j = 0; j < sc.n_species; ++j)
+                        atomicAdd(ea.g_vert + (long long)j * sc.V + vox, w * score_j(sc, ea, j, vox, cos_le, num));
+                }
+            }
+        }
+        if (on_target) phong_scores(ea.phong, cos_le, w, gk, gg);
+    }
+    if (act) {
+        own[vt.iv[i]] = own_acc;
+        if (single && acc != 0.0) atomicAdd(ea.g_vert + vox, acc);
+    }
+    if (sc.target >= 0) {
+        for (int o = 16; o > 0; o >>= 1) {
+            gk += __shfl_down_sync(0xffffffffu, gk, o);
+            gg += __shfl_down_sync(0xffffffffu, gg, o);
+        }
+        if ((threadIdx.x & 31) == 0 && (gk != 0.0 || gg != 0.0)) {
+            atomicAdd(ea.g_phong, gk);
+            atomicAdd(ea.g_phong + 1, gg);
+        }
+    }
+}
+
 // ------------------------------------------------------------------ K5a path suffix
 __global__ void __launch_bounds__(kTPB) k_path_gradient(const __grid_constant__ DScene sc,
                                                         const __grid_constant__ StoreView st,
@@ -665,9 +769,13 @@ cudaError_t launch_le_forward(const DScene& sc, const VertexTable& vt, const Eva
 }
 
 cudaError_t launch_le_gradient(const DScene& sc, const VertexTable& vt, const EvalArgs& ea, double* own,
-                               int hash_bits, int agg, int spread, int packet, cudaStream_t s,
-                               unsigned long long* launches) {
+                               int hash_bits, int agg, int spread, int packet, int tree,
+                               cudaStream_t s, unsigned long long* launches) {
     if (vt.n == 0) return cudaSuccess;
+    if (packet == 1 && hash_bits == 0 && agg == 0 && tree > 0) {
+        k_le_gradient_tree<<<grid_for((long long)vt.n, kWF), kWF, 0, s>>>(sc, vt, ea, own, spread, tree);
+        LAUNCH_DONE();
+    }
     if (packet > 1 && hash_bits == 0 && agg == 0) {
         const long long n_pk = ((long long)vt.n + packet - 1) / packet;
         if (packet == 2)

@@ -118,8 +118,9 @@ def test_sort_empty_store_rejected(ctx):
 
 
 # ---------------------------------------------------------------- K4/K5 on identical stores
-MAPPINGS = {"wavefront": dict(mode=0, packet=1), "wavefront_p2": dict(mode=0, packet=2),
-            "wavefront_p4": dict(mode=0, packet=4), "per_path": dict(mode=1, packet=1)}
+MAPPINGS = {"wavefront": dict(mode=0, packet=1, tree=0), "wavefront_p2": dict(mode=0, packet=2, tree=0),
+            "wavefront_p4": dict(mode=0, packet=4, tree=0),
+            "wavefront_tree2": dict(mode=0, packet=1, tree=2), "per_path": dict(mode=1, packet=1, tree=0)}
 
 
 @pytest.fixture(params=list(MAPPINGS))
@@ -130,6 +131,7 @@ def mode(ctx, request):
     yield request.param
     ctx.set_option("mode", 0)
     ctx.set_option("packet", 2)
+    ctx.set_option("tree", 0)
 
 
 @pytest.mark.parametrize("name", list(FIXTURES))
@@ -380,3 +382,74 @@ def test_nccl_communicator_path(golden_dir):
     assert grad_err(r.grad_beta, g["pert_w_grad"]) <= GRAD_TOL
     st.free()
     c.close()
+
+
+# ---------------------------------------------------------------- statistical parity (fresh MC)
+def test_recycling_unbiased_over_30_repetitions(ctx):
+    """acceptance.cpp:277-325 (c5): +1% on one voxel; recycled estimate from a store traced
+    at the reference vs a fresh render at the perturbed point, 30 independent repetitions
+    at N = 1e6: the mean gap lies within 3 standard errors."""
+    s = S.two_species_cube(np.full(64, 2.0), 4, 0.04, 8, 8)
+    t = np.full(64, 2.0)
+    t[21] *= 1.01
+    st_scene = S.two_species_cube(t, 4, 0.04, 8, 8)
+    n = 1_000_000
+    diffs = []
+    for r in range(30):
+        ctx.upload(s)
+        st = ctx.render(s, RenderOptions(n_paths=n, seed=10000 + r, keep_paths=True)).store
+        rec = ctx.recycled_render(s, st, S.ParamSet(t)).sum()
+        st.free()
+        ctx.upload(st_scene)
+        fresh = ctx.render(st_scene, RenderOptions(n_paths=n, seed=20000 + r)).images.sum()
+        diffs.append(rec - fresh)
+    d = np.asarray(diffs)
+    sem = d.std(ddof=1) / np.sqrt(len(d))
+    assert abs(d.mean()) <= 3.0 * sem, (d.mean(), sem)
+
+
+def test_fresh_render_matches_reference_statistically(ctx, ref):
+    """Fresh sampling parity against the reference sampler: independent seeds, image
+    totals agree within 4 combined standard errors, per-pixel z-scores <= 5 for pixels
+    above 1% of the maximum, and the path-size histograms agree (chi^2, p > 1e-3)."""
+    from scipy import stats
+    s = S.cloud_scene(8, 6, 6)
+    ctx.upload(s)
+    n, reps = 200_000, 8
+    g = np.array([ctx.render(s, RenderOptions(n_paths=n, seed=1000 + r)).images for r in range(reps)])
+    workers = os.cpu_count() or 1
+    c = np.array([ref.render(s, n, 5000 + r, workers=workers)[0] for r in range(reps)])
+    se = np.sqrt(g.sum(1).var(ddof=1) / reps + c.sum(1).var(ddof=1) / reps)
+    assert abs(g.sum(1).mean() - c.sum(1).mean()) <= 4 * se
+    mg, mc = g.mean(0), c.mean(0)
+    sp = np.sqrt(g.var(0, ddof=1) / reps + c.var(0, ddof=1) / reps)
+    big = mc > 0.01 * mc.max()
+    assert (np.abs(mg - mc)[big] / np.maximum(sp[big], 1e-300)).max() <= 5.0
+    # path-size (B) histograms: device store vs the reference sampler (C restatement)
+    from pyoracle import Port
+    st = ctx.render(s, RenderOptions(n_paths=n, seed=77, keep_paths=True)).store
+    bg = np.bincount(st.sizes().astype(np.int64))
+    _, _, ost = Port().render(s, n, 78)
+    bc = np.bincount(ost.sizes().astype(np.int64))
+    m = max(len(bg), len(bc))
+    bg, bc = np.pad(bg, (0, m - len(bg))), np.pad(bc, (0, m - len(bc)))
+    keep = (bg + bc) >= 10
+    table = np.vstack([bg[keep], bc[keep]])
+    assert stats.chi2_contingency(table)[1] > 1e-3
+
+
+def test_recycling_speed_benefit(ctx):
+    """acceptance.cpp:481-506 (c9): iterations per second with N_r = 30 are at least 2x
+    those with N_r = 1 (resampling every iteration)."""
+    import time
+    s = S.cloud_scene(16, 12, 12)
+    ctx.upload(s)
+    gt = ctx.render(s, RenderOptions(n_paths=200_000, seed=612)).images
+    init = S.ParamSet(np.full(16 ** 3, 1.5))
+    speed = {}
+    for nr in (30, 1):
+        t0 = time.perf_counter()
+        ctx.reconstruct(s, gt, init, n_paths=400_000, seed=41, recycle_period=nr, max_iterations=60,
+                        alpha=0.02)
+        speed[nr] = 60 / (time.perf_counter() - t0)
+    assert speed[30] >= 2.0 * speed[1], speed
