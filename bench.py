@@ -169,16 +169,10 @@ def run_ours(args):
     n_paths = int(args.paths or CONFIGS[cfg]["paths"])
     if args.mode is not None:
         ctx.set_option("mode", args.mode)
-    if args.hash_bits is not None:
-        ctx.set_option("hash_bits", args.hash_bits)
-    if args.agg is not None:
-        ctx.set_option("agg", args.agg)
     if args.spread is not None:
         ctx.set_option("spread", args.spread)
     if args.packet is not None:
         ctx.set_option("packet", args.packet)
-    if args.tree is not None:
-        ctx.set_option("tree", args.tree)
     ctx.upload(scene)
     t0 = time.time()
     rr = ctx.render(scene, RenderOptions(n_paths=n_paths, seed=7, keep_paths=True,
@@ -272,7 +266,7 @@ def run_ours(args):
                        "trace_s": round(t1 - t0, 3), "sort_s": round(t2 - t1, 3),
                        "sorted_by_B": not args.no_sort,
                        "mode": "per_path" if args.mode == 1 else "wavefront",
-                       "hash_bits": args.hash_bits, "agg": args.agg, "spread": args.spread, "packet": args.packet, "tree": args.tree,
+                       "spread": args.spread, "packet": args.packet,
                        "parallelism": f"paths sharded over {world} GPU(s), NCCL allreduce"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(),
@@ -362,11 +356,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sort", action="store_true", help="evaluate the unsorted (path-major) store")
     ap.add_argument("--mode", type=int, default=None, help="0 wavefront (default), 1 fused per-path")
-    ap.add_argument("--hash-bits", type=int, default=None, help="K5b smem hash bits (0 = direct atomics)")
-    ap.add_argument("--agg", type=int, default=None, help="warp-aggregated reductions (0 off, 1 match, 2 runs)")
     ap.add_argument("--spread", type=int, default=None, help="K5b lane spreading factor")
     ap.add_argument("--packet", type=int, default=None, help="K5b rays per thread in lockstep")
-    ap.add_argument("--tree", type=int, default=None, help="K5b shuffle-merge rounds (packet 1)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

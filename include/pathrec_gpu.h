@@ -150,8 +150,9 @@ int prc_gpu_ctx_create_rank(int device, int rank, int world, const void* nccl_id
 void prc_gpu_ctx_destroy(prc_gpu_ctx* ctx);
 int prc_gpu_ctx_rank(const prc_gpu_ctx* ctx, int* rank, int* world);
 /* Engine knobs: "mode" 0 = event-major wavefront over Morton-ordered interaction
- * vertices (default), 1 = fused thread-per-path; "hash_bits" (8..14) = size of the
- * gradient kernel's shared-memory accumulation hash. */
+ * vertices (default), 1 = fused thread-per-path (the paper's mapping); "packet" 1/2/4 =
+ * LE rays per thread walked in lockstep by the gradient kernel (default 2); "spread" =
+ * Morton distance between the packets of one warp (default 64). */
 int prc_gpu_ctx_set_option(prc_gpu_ctx* ctx, const char* key, int64_t value);
 
 /* Uploads (and validates, finalizes) the scene; replaces any previous scene and

@@ -105,11 +105,8 @@ struct prc_gpu_ctx {
     cudaStream_t stream = nullptr;
     unsigned long long launches = 0;
     int mode = 0;        // 0: event-major wavefront (default), 1: fused thread-per-path
-    int hash_bits = 0;   // K5b: 0 = direct fp64 L2 reductions (measured fastest); else smem hash 2^bits
     int spread = 64;     // K5b lane spreading factor (packet 2: 8 best at 1e7, 64-128 at 1e8)
     int packet = 2;      // K5b rays per thread walked in lockstep (measured best: 2)
-    int tree = 0;        // K5b (packet 1): shuffle-merge rounds (0..2)
-    int agg = 0;         // warp-aggregated reductions (match + fixed-point REDUX): measured slower, off
     // scene
     bool have_scene = false;
     DScene dsc{};
@@ -586,7 +583,7 @@ void run_forward(prc_gpu_ctx* c, prc_gpu_store* st, const Resolved& r, const Eva
     CK(cudaEventRecord(c->ev[1], q));
     if (c->mode == 0) {
         CK(launch_prefix(s, st->view(), ea, st->lp.p, q, &c->launches));
-        CK(launch_le_forward(s, vertex_table(st), ea, st->lp.p, c->agg, q, &c->launches));
+        CK(launch_le_forward(s, vertex_table(st), ea, st->lp.p, q, &c->launches));
     } else {
         CK(launch_forward(s, st->view(), ea, q, &c->launches));
     }
@@ -604,8 +601,7 @@ void run_gradient(prc_gpu_ctx* c, prc_gpu_store* st, const EvalArgs& ea) {
     CK(cudaMemsetAsync(c->g_vert.p, 0, c->g_vert.bytes(), q));
     CK(cudaMemsetAsync(c->g_phong.p, 0, 2 * sizeof(double), q));
     if (c->mode == 0) {
-        CK(launch_le_gradient(s, vertex_table(st), ea, st->own.p, c->hash_bits, c->agg, c->spread,
-                                  s.dda_packed ? c->packet : 1, c->tree, q,
+        CK(launch_le_gradient(s, vertex_table(st), ea, st->own.p, c->spread, s.dda_packed ? c->packet : 1, q,
                               &c->launches));
         CK(launch_path_gradient(s, st->view(), ea, st->own.p, q, &c->launches));
     } else {
@@ -1268,23 +1264,13 @@ PRC_EXPORT int prc_gpu_ctx_set_option(prc_gpu_ctx* ctx, const char* key, int64_t
     if (k == "mode") {
         if (value != 0 && value != 1) return fail(PRC_ERR_CONFIG, "mode must be 0 (wavefront) or 1 (path)");
         ctx->mode = (int)value;
-    } else if (k == "hash_bits") {
-        if (value != 0 && (value < 8 || value > 14))
-            return fail(PRC_ERR_CONFIG, "hash_bits must be 0 (direct atomics) or in 8..14");
-        ctx->hash_bits = (int)value;
     } else if (k == "spread") {
         if (value < 1 || value > 4096) return fail(PRC_ERR_CONFIG, "spread must be in 1..4096");
         ctx->spread = (int)value;
     } else if (k == "packet") {
-        if (value != 1 && value != 2 && value != 4 && value != 8)
-            return fail(PRC_ERR_CONFIG, "packet must be 1, 2, 4 or 8");
+        if (value != 1 && value != 2 && value != 4)
+            return fail(PRC_ERR_CONFIG, "packet must be 1, 2 or 4");
         ctx->packet = (int)value;
-    } else if (k == "tree") {
-        if (value < 0 || value > 2) return fail(PRC_ERR_CONFIG, "tree must be 0, 1 or 2");
-        ctx->tree = (int)value;
-    } else if (k == "agg") {
-        if (value < 0 || value > 2) return fail(PRC_ERR_CONFIG, "agg must be 0 (off), 1 (match) or 2 (runs)");
-        ctx->agg = (int)value;
     } else {
         return fail(PRC_ERR_CONFIG, "unknown option " + k);
     }

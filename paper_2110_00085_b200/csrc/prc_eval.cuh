@@ -118,81 +118,4 @@ __device__ __forceinline__ void phong_scores(const double* phong, double c, doub
 }
 
 
-// ---------------------------------------------------------------- warp-aggregated RED
-// Lanes of a warp in the event-major wavefront walk near-parallel rays from nearby
-// vertices, so at a given DDA iteration several lanes often sit in the same voxel.
-// agg_red() groups the lanes that are executing it together by key
-// (__match_any_sync) and sums each group exactly: every contribution is encoded in
-// fixed point against a warp-uniform scale 2^(56-E) (|x| < 2^56, so up to 32 of them
-// fit an int64) and split into three 21-bit limbs reduced with __reduce_add_sync
-// (REDUX).  One lane per group then issues a single fp64 reduction to L2.  Singleton
-// groups take the direct path with the unquantised value.
-struct WarpScale {
-    double scale, inv;  // 2^(56-E), 2^(E-56) with |every contribution| < 2^E
-};
-
-// Warp-uniform scale from each lane's bound |x| <= bound (call with all 32 lanes).
-__device__ __forceinline__ WarpScale warp_scale(double bound) {
-    double m = bound;
-    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-    int e = 0;
-    if (m > 0.0) frexp(m, &e);  // m < 2^e
-    WarpScale w;
-    w.scale = ldexp(1.0, 56 - e);
-    w.inv = ldexp(1.0, e - 56);
-    return w;
-}
-
-__device__ __forceinline__ void agg_red(double* base, unsigned key, double x, const WarpScale& ws) {
-    const unsigned act = __activemask();
-    const unsigned grp = __match_any_sync(act, key);
-    if ((grp & (grp - 1)) == 0) {  // singleton
-        atomicAdd(base + key, x);
-        return;
-    }
-    const long long q = __double2ll_rn(x * ws.scale);
-    const unsigned l0 = (unsigned)q & 0x1fffffu;
-    const unsigned l1 = (unsigned)(q >> 21) & 0x1fffffu;
-    const int l2 = (int)(q >> 42);
-    const unsigned s0 = __reduce_add_sync(grp, l0);
-    const unsigned s1 = __reduce_add_sync(grp, l1);
-    const int s2 = __reduce_add_sync(grp, l2);
-    if ((int)(threadIdx.x & 31) == __ffs(grp) - 1) {
-        const long long tot = ((long long)s2 << 42) + ((long long)s1 << 21) + (long long)s0;
-        atomicAdd(base + key, (double)tot * ws.inv);
-    }
-}
-
-// Run-based variant: only lanes adjacent in lane order with equal keys are combined
-// (Morton ordering puts vertices of one voxel in consecutive lanes, and their rays to
-// one camera advance through the same voxels).  Runs are found with one shuffle and a
-// ballot; no MATCH instruction.
-__device__ __forceinline__ void run_red(double* base, unsigned key, double x, const WarpScale& ws) {
-    const unsigned act = __activemask();
-    const int lane = threadIdx.x & 31;
-    const unsigned prev = __shfl_up_sync(act, key, 1);
-    const unsigned below = act & ((1u << lane) - 1u);                 // active lanes below me
-    const bool prev_act = lane > 0 && ((act >> (lane - 1)) & 1u);
-    const bool head = !(prev_act && prev == key);
-    const unsigned heads = __ballot_sync(act, head);
-    // run = [my head, next head) restricted to active lanes
-    const unsigned hb = heads & (below | (1u << lane));                // heads at or below me
-    const int my_head = 31 - __clz(hb);
-    const unsigned above = heads & ~((2u << lane) - 1u);               // heads strictly above me
-    const unsigned end_mask = above ? ((1u << (__ffs(above) - 1)) - 1u) : 0xffffffffu;
-    const unsigned run = act & end_mask & ~((1u << my_head) - 1u);
-    if ((run & (run - 1)) == 0) {  // singleton run
-        atomicAdd(base + key, x);
-        return;
-    }
-    const long long q = __double2ll_rn(x * ws.scale);
-    const unsigned s0 = __reduce_add_sync(run, (unsigned)q & 0x1fffffu);
-    const unsigned s1 = __reduce_add_sync(run, (unsigned)(q >> 21) & 0x1fffffu);
-    const int s2 = __reduce_add_sync(run, (int)(q >> 42));
-    if (lane == my_head) {
-        const long long tot = ((long long)s2 << 42) + ((long long)s1 << 21) + (long long)s0;
-        atomicAdd(base + key, (double)tot * ws.inv);
-    }
-}
-
 }  // namespace prc

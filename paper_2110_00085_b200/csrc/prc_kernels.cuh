@@ -158,15 +158,13 @@ cudaError_t launch_prefix(const DScene& sc, const StoreView& st, const EvalArgs&
                           cudaStream_t s, unsigned long long* launches);
 // K4b: per-event LE forward over the vertex table.
 cudaError_t launch_le_forward(const DScene& sc, const VertexTable& vt, const EvalArgs& ea,
-                              const double* lp, int agg, cudaStream_t s, unsigned long long* launches);
-// K5b: per-event LE gradient scatter (shared-memory hash, 2^hash_bits entries) and the
+                              const double* lp, cudaStream_t s, unsigned long long* launches);
+// K5b: per-event LE gradient scatter (fp64 L2 reductions; `packet` rays per thread in
+// lockstep with in-register voxel merging, lanes `spread` packets apart) and the
 // per-vertex event-weight sums own[iv].
-// agg != 0: warp-aggregated reductions (match + fixed-point REDUX) for the image
-// scatter (K4b) and the LE gradient scatter (K5b).
-// spread: lane-spreading factor of the K5b vertex assignment (1 = coherent warps).
 cudaError_t launch_le_gradient(const DScene& sc, const VertexTable& vt, const EvalArgs& ea,
-                               double* own, int hash_bits, int agg, int spread, int packet,
-                               int tree, cudaStream_t s, unsigned long long* launches);
+                               double* own, int spread, int packet, cudaStream_t s,
+                               unsigned long long* launches);
 // K5a: per-path suffix pass (segment spans, continuation scores) from own[iv].
 cudaError_t launch_path_gradient(const DScene& sc, const StoreView& st, const EvalArgs& ea,
                                  const double* own, cudaStream_t s, unsigned long long* launches);

@@ -8,8 +8,9 @@
 //                       log-prefix at every interaction vertex -> lp[iv]
 //   K4b k_le_forward    CTA per run of Morton-ordered interaction vertices, camera by
 //                       camera: LE transmittance, event value, image scatter, event cache
-//   K5b k_le_gradient   same mapping: w = value * residual, LE scatter -w*l into a
-//                       shared-memory hash (flushed once per camera), vertex score terms,
+//   K5b k_le_gradient_ms<2>  same vertex order: w = value * residual, LE scatter -w*l
+//                       with fp64 L2 reductions (two rays per thread in lockstep, spans in
+//                       the same voxel merged in registers), vertex score terms,
 //                       per-vertex weight sums own[iv]
 //   K5a k_path_gradient thread per path: suffix sums from own[iv] -> incoming-segment
 //                       spans and continuation score terms
@@ -25,7 +26,11 @@ namespace {
 
 constexpr int kWF = 256;  // vertices per CTA in the wavefront kernels
 constexpr int kTPB = 128;
-constexpr uint32_t kEmpty = 0xffffffffu;
+// Occupancy (measured on B200 at 1e8 paths): K4b at 4 CTAs x 256 threads (64 registers,
+// spills outside the DDA loop) beats 3 CTAs (80 registers) by 10%; K5b packets at 4 CTAs
+// x 128 threads (128 registers) beat 5-6 CTAs.
+constexpr int kFwdMinBlocks = 4;
+constexpr int kGradMinBlocks = 4;
 
 inline unsigned grid_for(long long n, int tpb) {
     long long g = (n + tpb - 1) / tpb;
@@ -145,13 +150,10 @@ __global__ void __launch_bounds__(kTPB) k_prefix(const __grid_constant__ DScene 
 }
 
 // ------------------------------------------------------------------ K4b LE forward
-#ifndef PRC_FWD_MINB
-#define PRC_FWD_MINB 4
-#endif
-__global__ void __launch_bounds__(kWF, PRC_FWD_MINB) k_le_forward(const __grid_constant__ DScene sc,
+__global__ void __launch_bounds__(kWF, kFwdMinBlocks) k_le_forward(const __grid_constant__ DScene sc,
                                                        const __grid_constant__ VertexTable vt,
                                                        const __grid_constant__ EvalArgs ea,
-                                                       const double* __restrict__ lp, int agg) {
+                                                       const double* __restrict__ lp) {
     const unsigned long long i = (unsigned long long)blockIdx.x * kWF + threadIdx.x;
     const bool act = i < vt.n;
     int vox = 0;
@@ -210,17 +212,7 @@ __global__ void __launch_bounds__(kWF, PRC_FWD_MINB) k_le_forward(const __grid_c
                 pix = -1;
             }
         }
-        if (agg) {  // image scatter, aggregated over lanes landing in the same pixel
-            const WarpScale ws = warp_scale(contrib);
-            if (contrib != 0.0) {
-                if (agg == 1)
-                    agg_red(ea.images + sc.det[k].img_off, (unsigned)pix, contrib, ws);
-                else
-                    run_red(ea.images + sc.det[k].img_off, (unsigned)pix, contrib, ws);
-            }
-        } else if (contrib != 0.0) {
-            atomicAdd(ea.images + sc.det[k].img_off + pix, contrib);
-        }
+        if (contrib != 0.0) atomicAdd(ea.images + sc.det[k].img_off + pix, contrib);
         if (act) {
             vt.ev_val[(unsigned long long)k * vt.n + i] = val;
             vt.ev_pix[(unsigned long long)k * vt.n + i] = pix;
@@ -231,36 +223,6 @@ __global__ void __launch_bounds__(kWF, PRC_FWD_MINB) k_le_forward(const __grid_c
 }
 
 // ------------------------------------------------------------------ K5b LE gradient
-// Shared-memory open-addressing hash (voxel -> partial dL/dbeta, fp32) with linear
-// probing; overflow falls through to a direct global atomic.  Flushed with fp64 global
-// atomics once per camera, so a CTA's ~256 coherent rays hit L2 once per distinct voxel.
-struct SmemHash {
-    uint32_t* keys;
-    float* vals;
-    uint32_t mask;
-    int shift;
-    __device__ __forceinline__ void add(uint32_t v, float x, double* g) {
-        uint32_t h = (v * 2654435761u) >> shift;
-#pragma unroll 1
-        for (int probe = 0; probe < 8; ++probe) {
-            const uint32_t k = ((volatile uint32_t*)keys)[h];
-            if (k == v) {
-                atomicAdd(vals + h, x);
-                return;
-            }
-            if (k == kEmpty) {
-                const uint32_t old = atomicCAS(keys + h, kEmpty, v);
-                if (old == kEmpty || old == v) {
-                    atomicAdd(vals + h, x);
-                    return;
-                }
-            }
-            h = (h + 1) & mask;
-        }
-        atomicAdd(g + v, (double)x);
-    }
-};
-
 __device__ __forceinline__ double score_j(const DScene& sc, const EvalArgs& ea, int j, int vox,
                                           double c, double num) {
     // score_term, pathstore.cpp:97-105, for species j (legacy: 1 / beta_t_tot)
@@ -271,26 +233,14 @@ __device__ __forceinline__ double score_j(const DScene& sc, const EvalArgs& ea, 
     return num > 0.0 ? sc.sp[j].albedo * phase_eval(sc.sp[j], c) / num : 0.0;
 }
 
-constexpr int kMaxAcc = 4;
-
+// One LE ray per thread, one fp64 L2 reduction per voxel visit (packet = 1).  Lane
+// spreading: within each chunk of 32*spread vertices, lane l of warp w takes vertex
+// l*spread + w, so one RED instruction touches 32 distinct Morton neighbourhoods instead
+// of (at high vertex density) one voxel 32 times.
 __global__ void __launch_bounds__(kWF, 3) k_le_gradient(const __grid_constant__ DScene sc,
                                                         const __grid_constant__ VertexTable vt,
                                                         const __grid_constant__ EvalArgs ea,
-                                                        double* __restrict__ own, int hash_bits, int agg,
-                                                        int spread) {
-    extern __shared__ uint32_t smem[];
-    const int H = 1 << hash_bits;
-    SmemHash hs{smem, reinterpret_cast<float*>(smem + H), (uint32_t)(H - 1), 32 - hash_bits};
-    const bool use_hash = ea.do_beta && sc.has_medium && hash_bits > 0;
-    const bool direct = ea.do_beta && sc.has_medium && hash_bits == 0;
-    if (use_hash)
-        for (int j = threadIdx.x; j < H; j += kWF) {
-            hs.keys[j] = kEmpty;
-            hs.vals[j] = 0.0f;
-        }
-    // Lane spreading: within each chunk of 32*spread vertices, lane l of warp w takes
-    // vertex l*spread + w, so one RED instruction touches 32 distinct Morton
-    // neighbourhoods instead of (at high vertex density) one voxel 32 times.
+                                                        double* __restrict__ own, int spread) {
     const unsigned long long g = (unsigned long long)blockIdx.x * kWF + threadIdx.x;
     unsigned long long i = g;
     if (spread > 1) {
@@ -299,23 +249,17 @@ __global__ void __launch_bounds__(kWF, 3) k_le_gradient(const __grid_constant__ 
         if (c0 + chunk <= vt.n) i = c0 + (g % 32ull) * spread + ((g / 32ull) % spread);
     }
     const bool act = i < vt.n;
-    V3 x = mk(0, 0, 0), d = mk(0, 0, 1);
     int vox = 0;
     uint32_t meta = 0;
     if (act) {
-        x = mk(vt.x[i], vt.y[i], vt.z[i]);
-        d = mk(vt.dx[i], vt.dy[i], vt.dz[i]);
         vox = vt.vox[i];
         meta = vt.meta[i];
     }
     const uint32_t kind = meta_kind(meta);
     const int surf = meta_surface(meta);
     const bool on_target = sc.target >= 0 && kind == VK_SURFACE && surf == sc.target;
-    const int n_out = ea.per_species ? sc.n_species : 1;
-    const double diag = 1.0000001 * sqrt(sc.vs[0] * sc.vs[0] + sc.vs[1] * sc.vs[1] + sc.vs[2] * sc.vs[2]);
-    double acc[kMaxAcc] = {0.0, 0.0, 0.0, 0.0};
-    double own_acc = 0.0, gk = 0.0, gg = 0.0;
-    if (use_hash) __syncthreads();
+    const bool single = !ea.per_species;
+    double own_acc = 0.0, acc = 0.0, gk = 0.0, gg = 0.0;
     for (int k = 0; k < sc.n_det; ++k) {
         double w = 0.0;
         if (act) {
@@ -325,76 +269,34 @@ __global__ void __launch_bounds__(kWF, 3) k_le_gradient(const __grid_constant__ 
                 w = ea.weights ? val * ea.weights[sc.det[k].img_off + pix] : val;
             }
         }
-        // warp-uniform fixed-point scale: |w * span| <= |w| * voxel diagonal
-        const WarpScale ws = warp_scale(fabs(w) * diag);
-        if (w != 0.0) {
-            own_acc += w;
-            V3 wd;
-            double r, geom, cos_le;
-            event_geometry(sc, sc.det[k], x, d, kind, surf, wd, r, geom, cos_le);
-            if (use_hash) {
-                const float cf = (float)(-w);
-                double* g = ea.g_span;
-                dda_walk(sc, x, wd, r, [&](int v, double ta, double tb) {
-                    hs.add((uint32_t)v, cf * (float)(tb - ta), g);
-                    return true;
-                });
-            } else if (direct && agg == 1) {  // warp-aggregated (MATCH) fp64 L2 reductions
-                const double cf = -w;
-                double* g = ea.g_span;
-                dda_walk(sc, x, wd, r, [&](int v, double ta, double tb) {
-                    agg_red(g, (unsigned)v, cf * (tb - ta), ws);
-                    return true;
-                });
-            } else if (direct && agg == 2) {  // adjacent-lane run aggregation
-                const double cf = -w;
-                double* g = ea.g_span;
-                dda_walk(sc, x, wd, r, [&](int v, double ta, double tb) {
-                    run_red(g, (unsigned)v, cf * (tb - ta), ws);
-                    return true;
-                });
-            } else if (direct) {  // one fp64 L2 reduction per voxel visit
-                const double cf = -w;
-                double* g = ea.g_span;
-                dda_walk(sc, x, wd, r, [&](int v, double ta, double tb) {
-                    atomicAdd(g + v, cf * (tb - ta));
-                    return true;
-                });
-            }
-            if (ea.do_beta && kind == VK_VOLUME) {
+        if (w == 0.0) continue;  // pathstore.cpp:197-198
+        own_acc += w;
+        const V3 x = mk(vt.x[i], vt.y[i], vt.z[i]);
+        V3 wd;
+        double r, geom, cos_le;
+        event_geometry(sc, sc.det[k], x, mk(vt.dx[i], vt.dy[i], vt.dz[i]), kind, surf, wd, r, geom, cos_le);
+        if (ea.do_beta) {
+            const double cf = -w;
+            double* gs = ea.g_span;
+            dda_walk(sc, x, wd, r, [&](int v, double ta, double tb) {
+                atomicAdd(gs + v, cf * (tb - ta));
+                return true;
+            });
+            if (kind == VK_VOLUME) {
                 const double num = ea.legacy ? 0.0 : scat_num(sc, ea.sp_t, vox, cos_le);
-                if (ea.per_species) {
-                    for (int j = 0; j < sc.n_species; ++j) {
-                        const double s = w * score_j(sc, ea, j, vox, cos_le, num);
-                        if (j < kMaxAcc)
-                            acc[j] += s;
-                        else
-                            atomicAdd(ea.g_vert + (long long)j * sc.V + vox, s);
-                    }
+                if (single) {
+                    acc += w * score_j(sc, ea, sc.unknown, vox, cos_le, num);
                 } else {
-                    acc[0] += w * score_j(sc, ea, sc.unknown, vox, cos_le, num);
+                    for (int j = 0; j < sc.n_species; ++j)
+                        atomicAdd(ea.g_vert + (long long)j * sc.V + vox, w * score_j(sc, ea, j, vox, cos_le, num));
                 }
             }
-            if (on_target) phong_scores(ea.phong, cos_le, w, gk, gg);
         }
-        if (use_hash) {  // flush this camera's partial gradients
-            __syncthreads();
-            for (int j = threadIdx.x; j < H; j += kWF) {
-                const uint32_t key = hs.keys[j];
-                if (key != kEmpty) {
-                    atomicAdd(ea.g_span + key, (double)hs.vals[j]);
-                    hs.keys[j] = kEmpty;
-                    hs.vals[j] = 0.0f;
-                }
-            }
-            __syncthreads();
-        }
+        if (on_target) phong_scores(ea.phong, cos_le, w, gk, gg);
     }
     if (act) {
         own[vt.iv[i]] = own_acc;
-        if (ea.do_beta && kind == VK_VOLUME)
-            for (int j = 0; j < n_out && j < kMaxAcc; ++j)
-                if (acc[j] != 0.0) atomicAdd(ea.g_vert + (long long)j * sc.V + vox, acc[j]);
+        if (single && acc != 0.0) atomicAdd(ea.g_vert + vox, acc);
     }
     if (sc.target >= 0) {
         for (int o = 16; o > 0; o >>= 1) {
@@ -416,10 +318,7 @@ __global__ void __launch_bounds__(kWF, 3) k_le_gradient(const __grid_constant__ 
 // (~0.35 per voxel visit for M = 4 at 1e8 paths), while `spread` keeps the 32 lanes of a
 // warp on distinct packets far apart in Morton order (no same-address RED conflicts).
 template <int M>
-#ifndef PRC_GRAD_MINB
-#define PRC_GRAD_MINB 4
-#endif
-__global__ void __launch_bounds__(128, M == 2 ? PRC_GRAD_MINB : 1) k_le_gradient_ms(const __grid_constant__ DScene sc,
+__global__ void __launch_bounds__(128, M == 2 ? kGradMinBlocks : 1) k_le_gradient_ms(const __grid_constant__ DScene sc,
                                                         const __grid_constant__ VertexTable vt,
                                                         const __grid_constant__ EvalArgs ea,
                                                         double* __restrict__ own, int spread) {
@@ -532,110 +431,6 @@ __global__ void __launch_bounds__(128, M == 2 ? PRC_GRAD_MINB : 1) k_le_gradient
         if (pk >= n_pk || i >= vt.n) continue;
         own[vt.iv[i]] = own_acc[r];
         if (single && acc[r] != 0.0) atomicAdd(ea.g_vert + vt.vox[i], acc[r]);
-    }
-    if (sc.target >= 0) {
-        for (int o = 16; o > 0; o >>= 1) {
-            gk += __shfl_down_sync(0xffffffffu, gk, o);
-            gg += __shfl_down_sync(0xffffffffu, gg, o);
-        }
-        if ((threadIdx.x & 31) == 0 && (gk != 0.0 || gg != 0.0)) {
-            atomicAdd(ea.g_phong, gk);
-            atomicAdd(ea.g_phong + 1, gg);
-        }
-    }
-}
-
-// ------------------------------------------------------------------ K5b, shuffle tree
-// One LE ray per thread on the lean single-ray walk.  Lanes come in groups of 4 that hold
-// consecutive Morton vertices (their rays to one camera advance through the same voxels
-// at the same iteration); groups are spread `spread` apart in Morton order.  At every
-// emitted span, `rounds` butterfly steps (lane^1, then lane^2) fold the partner's
-// contribution into the lower lane when both sit in the same voxel, so one REDG serves
-// the group.  Partners that are not emitting this iteration are not merged (exact).
-__device__ __forceinline__ void tree_red(double* g, int v, double x, int rounds) {
-    const unsigned act = __activemask();
-    const int lane = threadIdx.x & 31;
-    bool keep = true;
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-        if (r >= rounds) break;
-        const int m = 1 << r;
-        const int pv = __shfl_xor_sync(act, keep ? v : -1, m);
-        const double px = __shfl_xor_sync(act, x, m);
-        const bool pact = (act >> (lane ^ m)) & 1u;
-        if (keep && pact && pv == v) {
-            if (lane & m)
-                keep = false;
-            else
-                x += px;
-        }
-    }
-    if (keep) atomicAdd(g + v, x);
-}
-
-__global__ void __launch_bounds__(kWF, PRC_FWD_MINB) k_le_gradient_tree(
-    const __grid_constant__ DScene sc, const __grid_constant__ VertexTable vt,
-    const __grid_constant__ EvalArgs ea, double* __restrict__ own, int spread, int rounds) {
-    // group-granular spreading: lane l of warp w -> group (l/4)*spread + w, member l%4
-    const unsigned long long g = (unsigned long long)blockIdx.x * kWF + threadIdx.x;
-    unsigned long long i = g;
-    if (spread > 1) {
-        const unsigned long long chunk = 32ull * (unsigned long long)spread;
-        const unsigned long long c0 = (g / chunk) * chunk;
-        if (c0 + chunk <= vt.n) {
-            const unsigned long long lane = g % 32ull, w = (g / 32ull) % spread;
-            i = c0 + (((lane >> 2) * spread + w) << 2) + (lane & 3ull);
-        }
-    }
-    const bool act = i < vt.n;
-    int vox = 0;
-    uint32_t meta = 0;
-    if (act) {
-        vox = vt.vox[i];
-        meta = vt.meta[i];
-    }
-    const uint32_t kind = meta_kind(meta);
-    const int surf = meta_surface(meta);
-    const bool on_target = sc.target >= 0 && kind == VK_SURFACE && surf == sc.target;
-    const bool single = !ea.per_species;
-    double own_acc = 0.0, acc = 0.0, gk = 0.0, gg = 0.0;
-    for (int k = 0; k < sc.n_det; ++k) {
-        double w = 0.0;
-        if (act) {
-            const int pix = vt.ev_pix[(unsigned long long)k * vt.n + i];
-            if (pix >= 0) {
-                const double val = (double)vt.ev_val[(unsigned long long)k * vt.n + i];
-                w = ea.weights ? val * ea.weights[sc.det[k].img_off + pix] : val;
-            }
-        }
-        if (w == 0.0) continue;
-        own_acc += w;
-        const V3 x = mk(vt.x[i], vt.y[i], vt.z[i]);
-        V3 wd;
-        double r, geom, cos_le;
-        event_geometry(sc, sc.det[k], x, mk(vt.dx[i], vt.dy[i], vt.dz[i]), kind, surf, wd, r, geom, cos_le);
-        if (ea.do_beta) {
-            const double cf = -w;
-            double* gs = ea.g_span;
-            dda_walk(sc, x, wd, r, [&](int v, double ta, double tb) {
-                tree_red(gs, v, cf * (tb - ta), rounds);
-                return true;
-            });
-            if (kind == VK_VOLUME) {
-                const double num = ea.legacy ? 0.0 : scat_num(sc, ea.sp_t, vox, cos_le);
-                if (single) {
-                    acc += w * score_j(sc, ea, sc.unknown, vox, cos_le, num);
-                } else {
-                    for (int j = 0; j < sc.n_species; ++j)
-                        atomicAdd(ea.g_vert + (long long)j * sc.V + vox, w * score_j(sc, ea, j, vox, cos_le, num));
-                }
-            }
-        }
-        if (on_target) phong_scores(ea.phong, cos_le, w, gk, gg);
-    }
-    if (act) {
-        own[vt.iv[i]] = own_acc;
-        if (single && acc != 0.0) atomicAdd(ea.g_vert + vox, acc);
     }
     if (sc.target >= 0) {
         for (int o = 16; o > 0; o >>= 1) {
@@ -762,36 +557,24 @@ cudaError_t launch_prefix(const DScene& sc, const StoreView& st, const EvalArgs&
 }
 
 cudaError_t launch_le_forward(const DScene& sc, const VertexTable& vt, const EvalArgs& ea,
-                              const double* lp, int agg, cudaStream_t s, unsigned long long* launches) {
+                              const double* lp, cudaStream_t s, unsigned long long* launches) {
     if (vt.n == 0) return cudaSuccess;
-    k_le_forward<<<grid_for((long long)vt.n, kWF), kWF, 0, s>>>(sc, vt, ea, lp, agg);
+    k_le_forward<<<grid_for((long long)vt.n, kWF), kWF, 0, s>>>(sc, vt, ea, lp);
     LAUNCH_DONE();
 }
 
 cudaError_t launch_le_gradient(const DScene& sc, const VertexTable& vt, const EvalArgs& ea, double* own,
-                               int hash_bits, int agg, int spread, int packet, int tree,
-                               cudaStream_t s, unsigned long long* launches) {
+                               int spread, int packet, cudaStream_t s, unsigned long long* launches) {
     if (vt.n == 0) return cudaSuccess;
-    if (packet == 1 && hash_bits == 0 && agg == 0 && tree > 0) {
-        k_le_gradient_tree<<<grid_for((long long)vt.n, kWF), kWF, 0, s>>>(sc, vt, ea, own, spread, tree);
-        LAUNCH_DONE();
-    }
-    if (packet > 1 && hash_bits == 0 && agg == 0) {
+    if (packet > 1) {
         const long long n_pk = ((long long)vt.n + packet - 1) / packet;
         if (packet == 2)
             k_le_gradient_ms<2><<<grid_for(n_pk, 128), 128, 0, s>>>(sc, vt, ea, own, spread);
-        else if (packet == 4)
-            k_le_gradient_ms<4><<<grid_for(n_pk, 128), 128, 0, s>>>(sc, vt, ea, own, spread);
         else
-            k_le_gradient_ms<8><<<grid_for(n_pk, 128), 128, 0, s>>>(sc, vt, ea, own, spread);
+            k_le_gradient_ms<4><<<grid_for(n_pk, 128), 128, 0, s>>>(sc, vt, ea, own, spread);
         LAUNCH_DONE();
     }
-    const size_t smem = hash_bits > 0 ? (size_t)(1u << hash_bits) * 8u : 0;
-    if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(k_le_gradient, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-    }
-    k_le_gradient<<<grid_for((long long)vt.n, kWF), kWF, smem, s>>>(sc, vt, ea, own, hash_bits, agg, spread);
+    k_le_gradient<<<grid_for((long long)vt.n, kWF), kWF, 0, s>>>(sc, vt, ea, own, spread);
     LAUNCH_DONE();
 }
 

@@ -118,9 +118,8 @@ def test_sort_empty_store_rejected(ctx):
 
 
 # ---------------------------------------------------------------- K4/K5 on identical stores
-MAPPINGS = {"wavefront": dict(mode=0, packet=1, tree=0), "wavefront_p2": dict(mode=0, packet=2, tree=0),
-            "wavefront_p4": dict(mode=0, packet=4, tree=0),
-            "wavefront_tree2": dict(mode=0, packet=1, tree=2), "per_path": dict(mode=1, packet=1, tree=0)}
+MAPPINGS = {"wavefront": dict(mode=0, packet=1), "wavefront_p2": dict(mode=0, packet=2),
+            "wavefront_p4": dict(mode=0, packet=4), "per_path": dict(mode=1, packet=1)}
 
 
 @pytest.fixture(params=list(MAPPINGS))
@@ -131,7 +130,6 @@ def mode(ctx, request):
     yield request.param
     ctx.set_option("mode", 0)
     ctx.set_option("packet", 2)
-    ctx.set_option("tree", 0)
 
 
 @pytest.mark.parametrize("name", list(FIXTURES))
