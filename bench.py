@@ -194,7 +194,7 @@ def run_ours(args):
     # ---- timed region: exactly K recycled iterations
     barrier(pg)
     launches0 = ctx.kernel_launches()
-    fwd_ms = grad_ms = 0.0
+    fwd_ms = grad_ms = fwd_pp_ms = grad_pp_ms = 0.0
     with ClockSampler(local) as clk:
         ctx.timer_start()
         for _ in range(args.steps):
@@ -202,6 +202,8 @@ def run_ours(args):
             tm = ctx.last_timings()
             fwd_ms += tm["forward"]
             grad_ms += tm["gradient"]
+            fwd_pp_ms += tm["forward_per_path"]
+            grad_pp_ms += tm["gradient_per_path"]
         ms = ctx.timer_stop()
     barrier(pg)
     launches = ctx.kernel_launches() - launches0
@@ -210,6 +212,8 @@ def run_ours(args):
     value = seg_global / (ms_per_step / 1e3)
     fwd_ms /= args.steps
     grad_ms /= args.steps
+    fwd_pp_ms /= args.steps
+    grad_pp_ms /= args.steps
     # ---- roofline: algorithmic bytes per pass = 8 W_live + 64 V + 16 E
     W_live = stats["live_path_spans"] + stats["le_spans"]
     E = stats["events"]
@@ -223,7 +227,8 @@ def run_ours(args):
                 "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
                 "traffic": load_traffic(cfg), "bytes_per_launch": bytes_pass / world,
                 "launch_ms": round(dom_ms, 3), "forward_ms": round(fwd_ms, 3),
-                "gradient_ms": round(grad_ms, 3),
+                "gradient_ms": round(grad_ms, 3), "k_prefix_ms": round(fwd_pp_ms, 3),
+                "k_path_gradient_ms": round(grad_pp_ms, 3),
                 "iteration_roofline_seg_per_s": seg_global / (bytes_iter / (peak * 1e9) / world),
                 "iteration_frac": round(value / (seg_global / (bytes_iter / (peak * 1e9) / world)), 4)}
     # ---- e2e through the reference-facing API with host buffers

@@ -282,8 +282,9 @@ int prc_gpu_reconstruct(prc_gpu_ctx* ctx, const prc_gpu_params* initial, const d
 
 /* Milliseconds of the most recent evaluate / opt_step kernels, measured with CUDA
  * events on the launching stream: [0] prep, [1] forward (K4), [2] image allreduce +
- * loss, [3] gradient (K5), [4] grad allreduce + ADAM, [5] total. */
-int prc_gpu_last_timings(const prc_gpu_ctx* ctx, double* ms6);
+ * loss, [3] gradient (K5), [4] grad allreduce + ADAM, [5] total, [6] the per-path part of
+ * K4 (k_prefix), [7] the per-path part of K5 (k_path_gradient). */
+int prc_gpu_last_timings(const prc_gpu_ctx* ctx, double* ms8);
 /* CUDA events recorded on the context's stream: start / stop -> elapsed ms. */
 int prc_gpu_timer_start(prc_gpu_ctx* ctx);
 int prc_gpu_timer_stop(prc_gpu_ctx* ctx, double* ms);

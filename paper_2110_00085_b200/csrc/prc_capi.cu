@@ -105,6 +105,7 @@ struct prc_gpu_ctx {
     cudaStream_t stream = nullptr;
     unsigned long long launches = 0;
     int mode = 0;        // 0: event-major wavefront (default), 1: fused thread-per-path
+    bool timed_sub = false, timed_grad = false;  // sub-phase events recorded this call
     int spread = 64;     // K5b lane spreading factor (packet 2: 8 best at 1e7, 64-128 at 1e8)
     int packet = 2;      // K5b rays per thread walked in lockstep (measured best: 2)
     // scene
@@ -139,9 +140,9 @@ struct prc_gpu_ctx {
     const prc_gpu_store* last_fwd_store = nullptr;
     unsigned long long last_fwd_clamps = 0;
     // timing
-    cudaEvent_t ev[6] = {};
+    cudaEvent_t ev[9] = {};  // [0..5] phases, [6] after K4a, [7] before K5a, [8] spare
     cudaEvent_t timer[2] = {};
-    double last_ms[6] = {};
+    double last_ms[8] = {};
     ~prc_gpu_ctx() {
         if (cub_tmp) cudaFree(cub_tmp);
         for (auto& e : timer)
@@ -580,9 +581,12 @@ void run_forward(prc_gpu_ctx* c, prc_gpu_store* st, const Resolved& r, const Eva
     CK(cudaMemsetAsync(c->images.p, 0, c->images.bytes(), q));
     CK(cudaMemsetAsync(c->clamps.p, 0, sizeof(unsigned long long), q));
     ea = eval_args(c, st, er, phong_dev);
+    c->timed_sub = c->mode == 0;
+    c->timed_grad = false;
     CK(cudaEventRecord(c->ev[1], q));
     if (c->mode == 0) {
         CK(launch_prefix(s, st->view(), ea, st->lp.p, q, &c->launches));
+        CK(cudaEventRecord(c->ev[6], q));
         CK(launch_le_forward(s, vertex_table(st), ea, st->lp.p, q, &c->launches));
     } else {
         CK(launch_forward(s, st->view(), ea, q, &c->launches));
@@ -603,6 +607,8 @@ void run_gradient(prc_gpu_ctx* c, prc_gpu_store* st, const EvalArgs& ea) {
     if (c->mode == 0) {
         CK(launch_le_gradient(s, vertex_table(st), ea, st->own.p, c->spread, s.dda_packed ? c->packet : 1, q,
                               &c->launches));
+        CK(cudaEventRecord(c->ev[7], q));
+        c->timed_grad = true;
         CK(launch_path_gradient(s, st->view(), ea, st->own.p, q, &c->launches));
     } else {
         CK(launch_gradient(s, st->view(), ea, q, &c->launches));
@@ -639,6 +645,15 @@ void record_timings(prc_gpu_ctx* c) {
     }
     CK(cudaEventElapsedTime(&ms, c->ev[0], c->ev[5]));
     c->last_ms[5] = ms;
+    c->last_ms[6] = c->last_ms[7] = 0.0;
+    if (c->mode == 0 && c->timed_sub) {
+        CK(cudaEventElapsedTime(&ms, c->ev[1], c->ev[6]));
+        c->last_ms[6] = ms;
+        if (c->timed_grad) {
+            CK(cudaEventElapsedTime(&ms, c->ev[7], c->ev[4]));
+            c->last_ms[7] = ms;
+        }
+    }
 }
 
 // ----------------------------------------------------------------------- K1 trace
@@ -1668,9 +1683,9 @@ PRC_EXPORT int prc_gpu_reconstruct(prc_gpu_ctx* ctx, const prc_gpu_params* initi
     ABI_CATCH
 }
 
-PRC_EXPORT int prc_gpu_last_timings(const prc_gpu_ctx* ctx, double* ms6) {
-    if (!ctx || !ms6) return fail(PRC_ERR_INVALID, "null argument");
-    for (int i = 0; i < 6; ++i) ms6[i] = ctx->last_ms[i];
+PRC_EXPORT int prc_gpu_last_timings(const prc_gpu_ctx* ctx, double* ms8) {
+    if (!ctx || !ms8) return fail(PRC_ERR_INVALID, "null argument");
+    for (int i = 0; i < 8; ++i) ms8[i] = ctx->last_ms[i];
     return PRC_OK;
 }
 

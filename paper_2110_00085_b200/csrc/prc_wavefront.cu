@@ -97,6 +97,11 @@ __global__ void k_vt_gather(const __grid_constant__ StoreView st, const uint32_t
 }
 
 // ------------------------------------------------------------------ K4a prefix
+// Thread per path over the B-sorted store (the paper's Path Sorting mapping): the vertex
+// loop is warp-uniform and record loads are coalesced.  (Measured: the segment-queue
+// regeneration used by K5a is slower here, because a K4a step is only a gather + FMA.)
+__device__ __forceinline__ int warp_count(bool p) { return __popc(__ballot_sync(0xffffffffu, p)); }
+
 __global__ void __launch_bounds__(kTPB) k_prefix(const __grid_constant__ DScene sc,
                                                  const __grid_constant__ StoreView st,
                                                  const __grid_constant__ EvalArgs ea, double* lp) {
@@ -112,7 +117,6 @@ __global__ void __launch_bounds__(kTPB) k_prefix(const __grid_constant__ DScene 
     for (int b = 1; b < B; ++b) {
         const unsigned long long r = rb + (unsigned long long)b * rs;
         const unsigned long long iv = ib + (unsigned long long)(b - 1) * rs;
-        const V3 x = mk(st.px[r], st.py[r], st.pz[r]);
         if (dead) {
             lp[iv] = -INFINITY;
             continue;
@@ -145,7 +149,7 @@ __global__ void __launch_bounds__(kTPB) k_prefix(const __grid_constant__ DScene 
             else
                 l += log(PRC_PI * fr);
         }
-        xprev = x;
+        xprev = mk(st.px[r], st.py[r], st.pz[r]);
     }
 }
 
@@ -445,55 +449,81 @@ __global__ void __launch_bounds__(128, M == 2 ? kGradMinBlocks : 1) k_le_gradien
 }
 
 // ------------------------------------------------------------------ K5a path suffix
+// Thread per path (B-sorted).  Segment lengths (in voxels) are exponentially distributed,
+// so a warp walking "segment b of every lane" in lockstep idles most lanes.  Instead every
+// lane owns the queue of its path's segments: lanes step their current segment while at
+// least half the warp (or every lane that still has work) is walking, then all idle lanes
+// set up their next segment together (work regeneration; set-up cost is paid in batches).
+// from_here = W - prefix (suffix sums of pathstore.cpp:219-237 from own[iv]) weights the
+// incoming segment's spans; continuation score terms use after = W - prefix_next.
+template <bool PACKED>
 __global__ void __launch_bounds__(kTPB) k_path_gradient(const __grid_constant__ DScene sc,
                                                         const __grid_constant__ StoreView st,
                                                         const __grid_constant__ EvalArgs ea,
                                                         const double* __restrict__ own) {
     const long long p = path_index(st.n);
-    double gk = 0.0, gg = 0.0;
-    if (p >= 0) {
-        const int B = (int)st.B[p];
-        if (B >= 2) {
-            const unsigned long long rb = st.rec_base[p], ib = st.iv_base[p];
-            const unsigned rs = st.stride[p];
-            double W = 0.0;
-            bool any = false;
-            for (int b = 1; b < B; ++b) {
-                const double o = own[ib + (unsigned long long)(b - 1) * rs];
-                W += o;
-                any |= o != 0.0;
+    const int B = p >= 0 ? (int)st.B[p] : 0;
+    unsigned long long rb = 0, ib = 0;
+    unsigned rs = 0;
+    double W = 0.0;
+    bool any = false;
+    if (B >= 2) {
+        rb = st.rec_base[p];
+        ib = st.iv_base[p];
+        rs = st.stride[p];
+        for (int b = 1; b < B; ++b) {
+            const double o = own[ib + (unsigned long long)(b - 1) * rs];
+            W += o;
+            any |= o != 0.0;
+        }
+    }
+    V3 xprev = any ? mk(st.px[rb], st.py[rb], st.pz[rb]) : mk(0, 0, 0);
+    int b = 1;
+    bool done = !any;
+    double prefix = 0.0, cf = 0.0, gk = 0.0, gg = 0.0;
+    DdaState S;
+    S.alive = false;
+    const int nx = sc.dims[0], ny = sc.dims[1], nz = sc.dims[2];
+    double* g = ea.g_span;
+    for (;;) {
+        while (!done && !S.alive) {
+            if (b >= B) {
+                done = true;
+                break;
             }
-            if (any) {
-                V3 xprev = mk(st.px[rb], st.py[rb], st.pz[rb]);
-                double prefix = 0.0;
-                for (int b = 1; b < B; ++b) {
-                    const unsigned long long r = rb + (unsigned long long)b * rs;
-                    const double o = own[ib + (unsigned long long)(b - 1) * rs];
-                    const double from_here = W - prefix;  // suffix sums of pathstore.cpp:219-237
-                    const double prefix_next = prefix + o;
-                    const double after = W - prefix_next;
-                    const V3 x = mk(st.px[r], st.py[r], st.pz[r]);
-                    if (from_here != 0.0 && ea.do_beta) {
-                        const double cf = -from_here;
-                        double* g = ea.g_span;
-                        dda_walk(sc, xprev, mk(st.dx[r], st.dy[r], st.dz[r]), st.tt[r],
-                                 [&](int v, double ta, double tb) {
-                                     atomicAdd(g + v, cf * (tb - ta));
-                                     return true;
-                                 });
-                    }
-                    if (after != 0.0) {
-                        const uint32_t m = st.meta[r];
-                        const uint32_t kind = meta_kind(m);
-                        if (kind == VK_VOLUME && ea.do_beta) vertex_scores(sc, ea, st.vox[r], st.ct[r], after);
-                        if (sc.target >= 0 && kind == VK_SURFACE && meta_surface(m) == sc.target)
-                            phong_scores(ea.phong, st.ct[r], after, gk, gg);
-                    }
-                    prefix = prefix_next;
-                    xprev = x;
+            const unsigned long long r = rb + (unsigned long long)b * rs;
+            const double o = own[ib + (unsigned long long)(b - 1) * rs];
+            const double from_here = W - prefix;
+            const double prefix_next = prefix + o;
+            const double after = W - prefix_next;
+            if (after != 0.0) {
+                const uint32_t m = st.meta[r];
+                const uint32_t kind = meta_kind(m);
+                if (kind == VK_VOLUME && ea.do_beta) vertex_scores(sc, ea, st.vox[r], st.ct[r], after);
+                if (sc.target >= 0 && kind == VK_SURFACE && meta_surface(m) == sc.target)
+                    phong_scores(ea.phong, st.ct[r], after, gk, gg);
+            }
+            if (from_here != 0.0 && ea.do_beta) {
+                S.init(sc, xprev, mk(st.dx[r], st.dy[r], st.dz[r]), st.tt[r]);
+                cf = -from_here;
+            }
+            prefix = prefix_next;
+            xprev = mk(st.px[r], st.py[r], st.pz[r]);
+            ++b;
+        }
+        const int walking = warp_count(S.alive);
+        if (walking == 0 && warp_count(!done) == 0) break;
+        const int target = min(16, warp_count(!done));
+        do {  // 4 steps between warp votes
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (S.alive) {
+                    double len;
+                    const int v = dda_step_len<PACKED>(S, nx, ny, nz, len);
+                    if (v >= 0) atomicAdd(g + v, cf * len);
                 }
             }
-        }
+        } while (warp_count(S.alive) >= target && target > 0);
     }
     if (sc.target >= 0) {
         for (int o = 16; o > 0; o >>= 1) {
@@ -581,6 +611,9 @@ cudaError_t launch_le_gradient(const DScene& sc, const VertexTable& vt, const Ev
 cudaError_t launch_path_gradient(const DScene& sc, const StoreView& st, const EvalArgs& ea,
                                  const double* own, cudaStream_t s, unsigned long long* launches) {
     if (st.n == 0) return cudaSuccess;
-    k_path_gradient<<<grid_for((long long)st.n, kTPB), kTPB, 0, s>>>(sc, st, ea, own);
+    if (sc.dda_packed)
+        k_path_gradient<true><<<grid_for((long long)st.n, kTPB), kTPB, 0, s>>>(sc, st, ea, own);
+    else
+        k_path_gradient<false><<<grid_for((long long)st.n, kTPB), kTPB, 0, s>>>(sc, st, ea, own);
     LAUNCH_DONE();
 }

@@ -392,10 +392,10 @@ class Context:
 
     # ------------------------------------------------------------------ diagnostics
     def last_timings(self) -> dict:
-        ms = np.zeros(6)
+        ms = np.zeros(8)
         _check(_lib.prc_gpu_last_timings(self.ptr, _ptr(ms, _dp)))
         return dict(zip(["prep", "forward", "image_allreduce", "gradient", "grad_allreduce_adam",
-                         "total"], ms.tolist()))
+                         "total", "forward_per_path", "gradient_per_path"], ms.tolist()))
 
     def timer_start(self):
         _check(_lib.prc_gpu_timer_start(self.ptr))

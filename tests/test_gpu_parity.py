@@ -451,3 +451,33 @@ def test_recycling_speed_benefit(ctx):
                         alpha=0.02)
         speed[nr] = 60 / (time.perf_counter() - t0)
     assert speed[30] >= 2.0 * speed[1], speed
+
+
+def test_large_grid_unpacked_dda_paths(ctx, port, tmp_path):
+    """Grids wider than 512 voxels take the generic (unpacked) bounds check in every
+    DDA user: trace, K4a/K5a stepper, K4b/K5b walks.  Parity against the oracle on the
+    identical exported store, and bit-exact spans."""
+    g = S.Grid((520, 4, 4), (0.0, 0.0, 0.0), (1.0 / 520, 0.25, 0.25))
+    beta = 2.0 + np.sin(np.arange(g.voxel_count) * 0.01)
+    s = S.Scene(grid=g, species=[S.Species(beta, 0.9, "hg", 0.6, True)],
+                light=S.Light("point", (0.5, 0.5, 0.5), (0, 0, -1), 1.0),
+                detectors=[S.top_detector(6, 6), S.Detector((2.5, 0.5, 0.5), (-1, 0, 0), (0, 0, 1), 5, 5, 0.7)])
+    ctx.upload(s)
+    rays = np.random.default_rng(9).uniform(0, 1, size=(500, 7))
+    rays[:, 3:6] -= 0.5
+    rays[:, 3:6] /= np.linalg.norm(rays[:, 3:6], axis=1, keepdims=True)
+    rays[:, 6] *= 2.0
+    c1, v1, l1 = ctx.debug_walk(rays)
+    c2, v2, l2 = port.walk(s, rays)
+    assert np.array_equal(c1, c2) and np.array_equal(v1, v2)
+    assert np.array_equal(l1.view(np.uint64), l2.view(np.uint64))
+    st = ctx.render(s, RenderOptions(n_paths=3000, seed=4, keep_paths=True)).store
+    ctx.sort_by_size(st)
+    st.save(str(tmp_path / "big.pstr"))
+    ost = port.load(str(tmp_path / "big.pstr"))
+    t = perturbed(s)
+    w = np.linspace(-1.0, 2.0, s.pixel_count)
+    a = ctx.evaluate_store(s, st, t, EvalOptions(want_grad=True, pixel_weights=w))
+    b = port.evaluate(s, ost, t, abi.PRC_EVAL_NORMALIZE | abi.PRC_EVAL_WANT_GRAD, w)
+    assert img_err(a.images, b["images"]) <= IMG_TOL
+    assert grad_err(a.grad_beta, b["grad"]) <= GRAD_TOL
