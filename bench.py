@@ -35,7 +35,7 @@ CONFIGS = {
     "b": dict(n=128, rows=128, two=False, paths=100_000_000,
               desc="synthetic 128^3 single-type cloud, 9 cameras 128x128, 1e8 paths, sort+recycle render+gradient"),
     "c": dict(n=128, rows=128, two=True, paths=100_000_000,
-              desc="2-species 128^3 cloud (HG 0.85 + Rayleigh), 9 cameras 128x128, 1e8 paths"),
+              desc="2-species 128^3 cloud (HG 0.85 + Rayleigh), 9 cameras 128x128, 1e8 paths, per-type gradients"),
     "d": dict(n=0, rows=256, two=False, paths=10_000_000,
               desc="reflectometry: Phong sphere + 14 diffuse spheres in a Phong box, 16 views 256x256, 1e7 paths"),
 }
@@ -169,6 +169,8 @@ def run_ours(args):
     n_paths = int(args.paths or CONFIGS[cfg]["paths"])
     if args.mode is not None:
         ctx.set_option("mode", args.mode)
+    if CONFIGS[cfg]["two"]:
+        ctx.set_option("per_species", 1)  # config (c): per-type gradients every iteration
     if args.spread is not None:
         ctx.set_option("spread", args.spread)
     if args.packet is not None:

@@ -152,7 +152,9 @@ int prc_gpu_ctx_rank(const prc_gpu_ctx* ctx, int* rank, int* world);
 /* Engine knobs: "mode" 0 = event-major wavefront over Morton-ordered interaction
  * vertices (default), 1 = fused thread-per-path (the paper's mapping); "packet" 1/2/4 =
  * LE rays per thread walked in lockstep by the gradient kernel (default 2); "spread" =
- * Morton distance between the packets of one warp (default 64). */
+ * Morton distance between the packets of one warp (default 64); "per_species" 1 = the
+ * device-resident iteration (prc_gpu_opt_step) computes per-type gradients of every
+ * species (config (c)); the optimiser still updates the unknown species. */
 int prc_gpu_ctx_set_option(prc_gpu_ctx* ctx, const char* key, int64_t value);
 
 /* Uploads (and validates, finalizes) the scene; replaces any previous scene and

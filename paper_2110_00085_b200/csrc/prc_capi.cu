@@ -107,6 +107,7 @@ struct prc_gpu_ctx {
     int mode = 0;        // 0: event-major wavefront (default), 1: fused thread-per-path
     bool timed_sub = false, timed_grad = false;  // sub-phase events recorded this call
     int spread = 64;     // K5b lane spreading factor (packet 2: 8 best at 1e7, 64-128 at 1e8)
+    int opt_per_species = 0;  // opt_step computes per-type gradients of every species
     int packet = 2;      // K5b rays per thread walked in lockstep (measured best: 2)
     // scene
     bool have_scene = false;
@@ -1282,9 +1283,10 @@ PRC_EXPORT int prc_gpu_ctx_set_option(prc_gpu_ctx* ctx, const char* key, int64_t
     } else if (k == "spread") {
         if (value < 1 || value > 4096) return fail(PRC_ERR_CONFIG, "spread must be in 1..4096");
         ctx->spread = (int)value;
+    } else if (k == "per_species") {
+        ctx->opt_per_species = value ? 1 : 0;
     } else if (k == "packet") {
-        if (value != 1 && value != 2 && value != 4)
-            return fail(PRC_ERR_CONFIG, "packet must be 1, 2 or 4");
+        if (value < 1 || value > 4) return fail(PRC_ERR_CONFIG, "packet must be in 1..4");
         ctx->packet = (int)value;
     } else {
         return fail(PRC_ERR_CONFIG, "unknown option " + k);
@@ -1573,15 +1575,19 @@ static double opt_step(prc_gpu_ctx* c, prc_gpu_store* st) {
     CK(cudaMemsetAsync(c->loss.p, 0, 8, q));
     CK(launch_loss_residual(c->images.p, c->opt_gt.p, c->n_pix, c->weights.p, c->loss.p, q, &c->launches));
     ea.weights = c->weights.p;  // K5 with residual weights (+ gradient allreduce)
-    ea.do_beta = s.has_medium && s.unknown >= 0 ? 1 : 0;
+    ea.per_species = c->opt_per_species && s.has_medium ? 1 : 0;
+    ea.do_beta = s.has_medium && (s.unknown >= 0 || ea.per_species) ? 1 : 0;
     run_gradient(c, st, ea);
     ++c->opt_t;
     const double c1 = 1.0 - std::pow(c->adam.eta1, (double)c->opt_t);
     const double c2 = 1.0 - std::pow(c->adam.eta2, (double)c->opt_t);
     const double* g;
     if (c->opt_mode == 0) {
-        CK(launch_combine_grad(c->g_span.p, c->g_vert.p, 1, c->V, scale, c->g_out.p, q, &c->launches));
-        g = c->g_out.p;
+        // per-type mode (config (c)): grad_j = g_span + g_vert[j] for every species j;
+        // the optimiser updates the unknown species' slice
+        const int n_out = ea.per_species ? s.n_species : 1;
+        CK(launch_combine_grad(c->g_span.p, c->g_vert.p, n_out, c->V, scale, c->g_out.p, q, &c->launches));
+        g = c->g_out.p + (ea.per_species ? (size_t)s.unknown * c->V : 0);
     } else {
         CK(launch_scale(c->g_phong.p, 2, scale, q, &c->launches));
         g = c->g_phong.p;

@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(kWF, 3) k_le_gradient(const __grid_constant__ 
 // (~0.35 per voxel visit for M = 4 at 1e8 paths), while `spread` keeps the 32 lanes of a
 // warp on distinct packets far apart in Morton order (no same-address RED conflicts).
 template <int M>
-__global__ void __launch_bounds__(128, M == 2 ? kGradMinBlocks : 1) k_le_gradient_ms(const __grid_constant__ DScene sc,
+__global__ void __launch_bounds__(128, M == 2 ? kGradMinBlocks : (M == 3 ? 3 : 1)) k_le_gradient_ms(const __grid_constant__ DScene sc,
                                                         const __grid_constant__ VertexTable vt,
                                                         const __grid_constant__ EvalArgs ea,
                                                         double* __restrict__ own, int spread) {
@@ -600,6 +600,8 @@ cudaError_t launch_le_gradient(const DScene& sc, const VertexTable& vt, const Ev
         const long long n_pk = ((long long)vt.n + packet - 1) / packet;
         if (packet == 2)
             k_le_gradient_ms<2><<<grid_for(n_pk, 128), 128, 0, s>>>(sc, vt, ea, own, spread);
+        else if (packet == 3)
+            k_le_gradient_ms<3><<<grid_for(n_pk, 128), 128, 0, s>>>(sc, vt, ea, own, spread);
         else
             k_le_gradient_ms<4><<<grid_for(n_pk, 128), 128, 0, s>>>(sc, vt, ea, own, spread);
         LAUNCH_DONE();

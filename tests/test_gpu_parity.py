@@ -481,3 +481,22 @@ def test_large_grid_unpacked_dda_paths(ctx, port, tmp_path):
     b = port.evaluate(s, ost, t, abi.PRC_EVAL_NORMALIZE | abi.PRC_EVAL_WANT_GRAD, w)
     assert img_err(a.images, b["images"]) <= IMG_TOL
     assert grad_err(a.grad_beta, b["grad"]) <= GRAD_TOL
+
+
+def test_opt_step_per_type_mode_matches_single_unknown(ctx, golden_dir):
+    """Config (c): with per-type gradients on, the device iteration still moves the unknown
+    species exactly as the single-unknown iteration does (its gradient is the same)."""
+    scene = FIXTURES["tomo2"]["scene"]()
+    g = golden("tomo2")
+    ctx.upload(scene)
+    st = ctx.load_store(str(golden_dir / "tomo2.pstr"))
+    t = perturbed(scene)
+    gt = g["pert_res_images"] - weight_patterns(scene)["res"]
+    out = []
+    for ps in (0, 1):
+        ctx.set_option("per_species", ps)
+        ctx.opt_init(t, gt, alpha=0.05)
+        ctx.opt_step(st)
+        out.append(ctx.opt_params().beta)
+    ctx.set_option("per_species", 0)
+    assert np.abs(out[0] - out[1]).max() <= 1e-9 + 1e-6 * 0.05
