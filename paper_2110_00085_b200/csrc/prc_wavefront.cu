@@ -197,13 +197,7 @@ __global__ void __launch_bounds__(kWF, kFwdMinBlocks) k_le_forward(const __grid_
                 }
                 if (logval != -INFINITY) {
                     if (sc.has_medium) {
-                        double od = 0.0;
-                        const float* bt = ea.bt_tot;
-                        dda_walk(sc, x, w, r, [&](int v, double ta, double tb) {
-                            od = fma((double)__ldg(bt + v), tb - ta, od);
-                            return true;
-                        });
-                        logval -= od;
+                        logval -= dda_optical_depth(sc, x, w, r, ea.bt_tot);
                     }
                     if (logval > PRC_LOG_CLAMP || logval < -PRC_LOG_CLAMP) {
                         logval = clampd(logval, -PRC_LOG_CLAMP, PRC_LOG_CLAMP);
@@ -344,7 +338,7 @@ __global__ void __launch_bounds__(128, M == 2 ? kGradMinBlocks : (M == 3 ? 3 : 1
         double cf[M];
 #pragma unroll
         for (int r = 0; r < M; ++r) {
-            S[r].alive = false;
+            S[r] = DdaState{};  // dead: the branch-free step advances it harmlessly
             cf[r] = 0.0;
             const unsigned long long i = pk * M + r;
             if (pk >= n_pk || i >= vt.n) continue;
@@ -383,17 +377,14 @@ __global__ void __launch_bounds__(128, M == 2 ? kGradMinBlocks : (M == 3 ? 3 : 1
         const int nx = sc.dims[0], ny = sc.dims[1], nz = sc.dims[2];
         double* g = ea.g_span;
         if (M == 2) {  // hand-scheduled pair
-            while (S[0].alive || S[1].alive) {
-                double l0 = 0.0, l1 = 0.0;
-                const int v0 = S[0].alive ? dda_step_len(S[0], nx, ny, nz, l0) : -1;
-                const int v1 = S[1].alive ? dda_step_len(S[1], nx, ny, nz, l1) : -1;
-                const double x0 = cf[0] * l0, x1 = cf[1] * l1;
-                if (v0 >= 0 && v0 == v1) {
-                    atomicAdd(g + v0, x0 + x1);
-                } else {
-                    if (v0 >= 0) atomicAdd(g + v0, x0);
-                    if (v1 >= 0) atomicAdd(g + v1, x1);
-                }
+            while (S[0].alive || S[1].alive) {  // packets are only used on packed grids
+                double l0, l1;
+                const int v0 = dda_step_packed(S[0], l0);
+                const int v1 = dda_step_packed(S[1], l1);
+                const double x1 = cf[1] * l1;
+                const bool same = v0 >= 0 && v0 == v1;
+                if (v0 >= 0) atomicAdd(g + v0, cf[0] * l0 + (same ? x1 : 0.0));
+                if (v1 >= 0 && !same) atomicAdd(g + v1, x1);
             }
         } else {
             bool any = false;
@@ -481,8 +472,7 @@ __global__ void __launch_bounds__(kTPB) k_path_gradient(const __grid_constant__ 
     int b = 1;
     bool done = !any;
     double prefix = 0.0, cf = 0.0, gk = 0.0, gg = 0.0;
-    DdaState S;
-    S.alive = false;
+    DdaState S{};  // dead until the first segment is set up
     const int nx = sc.dims[0], ny = sc.dims[1], nz = sc.dims[2];
     double* g = ea.g_span;
     for (;;) {
@@ -517,11 +507,10 @@ __global__ void __launch_bounds__(kTPB) k_path_gradient(const __grid_constant__ 
         do {  // 4 steps between warp votes
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                if (S.alive) {
-                    double len;
-                    const int v = dda_step_len<PACKED>(S, nx, ny, nz, len);
-                    if (v >= 0) atomicAdd(g + v, cf * len);
-                }
+                double len;
+                const int v = PACKED ? dda_step_packed(S, len)
+                                     : (S.alive ? dda_step_len<false>(S, nx, ny, nz, len) : -1);
+                if (v >= 0) atomicAdd(g + v, cf * len);
             }
         } while (warp_count(S.alive) >= target && target > 0);
     }
