@@ -150,8 +150,8 @@ int prc_gpu_ctx_create_rank(int device, int rank, int world, const void* nccl_id
 void prc_gpu_ctx_destroy(prc_gpu_ctx* ctx);
 int prc_gpu_ctx_rank(const prc_gpu_ctx* ctx, int* rank, int* world);
 /* Engine knobs: "mode" 0 = event-major wavefront over Morton-ordered interaction
- * vertices (default), 1 = fused thread-per-path (the paper's mapping); "packet" 1/2/4 =
- * LE rays per thread walked in lockstep by the gradient kernel (default 2); "spread" =
+ * vertices (default), 1 = fused thread-per-path (the paper's mapping); "packet" 1..4 =
+ * LE rays per thread walked in lockstep by the gradient kernel (default 3); "spread" =
  * Morton distance between the packets of one warp (default 64); "per_species" 1 = the
  * device-resident iteration (prc_gpu_opt_step) computes per-type gradients of every
  * species (config (c)); the optimiser still updates the unknown species. */

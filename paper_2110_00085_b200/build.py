@@ -33,32 +33,41 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, defines=(), out: str = OUT) -> str:
+    """defines/out: A/B experiment builds (-D overrides into a separate .so)."""
+    if out == OUT and not defines and not force and not _stale():
         return OUT
+    tag = "" if out == OUT else "." + os.path.basename(out).replace(".so", "")
     objs = []
     for s in SOURCES:
-        obj = os.path.join(SRC, s.replace(".cu", ".o"))
-        cmd = [NVCC, *FLAGS, "-c", os.path.join(SRC, s), "-o", obj]
+        obj = os.path.join(SRC, s.replace(".cu", tag + ".o"))
+        cmd = [NVCC, *FLAGS, *("-D" + d for d in defines), "-c", os.path.join(SRC, s), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError(f"nvcc failed on {s}")
         if verbose:
             sys.stderr.write(r.stderr)
-        with open(os.path.join(SRC, s.replace(".cu", ".ptxas.txt")), "w") as f:
-            f.write(r.stderr)
+        if not tag:
+            with open(os.path.join(SRC, s.replace(".cu", ".ptxas.txt")), "w") as f:
+                f.write(r.stderr)
         objs.append(obj)
-    tmp = OUT + ".tmp"
+    tmp = out + ".tmp"
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs,
            "-lnccl", "-Xlinker", "-rpath,/usr/lib/x86_64-linux-gnu"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc link failed")
-    os.replace(tmp, OUT)
-    return OUT
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    # python build.py [--force] [-v] [--out PATH -DNAME=VALUE ...]
+    args = sys.argv[1:]
+    out = OUT
+    if "--out" in args:
+        out = os.path.abspath(args[args.index("--out") + 1])
+    defs = [a[2:] for a in args if a.startswith("-D")]
+    print(build(force="--force" in args, verbose="-v" in args, defines=defs, out=out))

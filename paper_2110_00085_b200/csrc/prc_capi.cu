@@ -108,7 +108,7 @@ struct prc_gpu_ctx {
     bool timed_sub = false, timed_grad = false;  // sub-phase events recorded this call
     int spread = 64;     // K5b lane spreading factor (packet 2: 8 best at 1e7, 64-128 at 1e8)
     int opt_per_species = 0;  // opt_step computes per-type gradients of every species
-    int packet = 2;      // K5b rays per thread walked in lockstep (measured best: 2)
+    int packet = 3;      // K5b rays per thread walked in lockstep (measured best: 3)
     // scene
     bool have_scene = false;
     DScene dsc{};

@@ -26,11 +26,23 @@ namespace {
 
 constexpr int kWF = 256;  // vertices per CTA in the wavefront kernels
 constexpr int kTPB = 128;
-// Occupancy (measured on B200 at 1e8 paths): K4b at 4 CTAs x 256 threads (64 registers,
-// spills outside the DDA loop) beats 3 CTAs (80 registers) by 10%; K5b packets at 4 CTAs
-// x 128 threads (128 registers) beat 5-6 CTAs.
-constexpr int kFwdMinBlocks = 4;
-constexpr int kGradMinBlocks = 4;
+// Occupancy (measured on B200 at 1e8 paths, config (b)): K4b at 6 CTAs x 256 threads
+// (40 registers, spills outside the DDA loop) 604 ms vs 5 CTAs 613, 4 CTAs 639, 3 CTAs
+// 714; K5b packet-3 at 4 CTAs x 128 threads (128 registers) 937 ms vs 3 CTAs 977, 2 CTAs
+// 977, 5 CTAs 1102; packet 2 (4 CTAs) 1108, packet 4 (3 CTAs) 1132.
+#ifndef PRC_FWD_MINB  // -D overrides are for A/B builds (scripts/build_variant.sh)
+#define PRC_FWD_MINB 6
+#endif
+#ifndef PRC_GRAD2_MINB
+#define PRC_GRAD2_MINB 4
+#endif
+#ifndef PRC_GRAD3_MINB
+#define PRC_GRAD3_MINB 4
+#endif
+#ifndef PRC_GRAD4_MINB
+#define PRC_GRAD4_MINB 1
+#endif
+constexpr int kFwdMinBlocks = PRC_FWD_MINB;
 
 inline unsigned grid_for(long long n, int tpb) {
     long long g = (n + tpb - 1) / tpb;
@@ -316,7 +328,7 @@ __global__ void __launch_bounds__(kWF, 3) k_le_gradient(const __grid_constant__ 
 // (~0.35 per voxel visit for M = 4 at 1e8 paths), while `spread` keeps the 32 lanes of a
 // warp on distinct packets far apart in Morton order (no same-address RED conflicts).
 template <int M>
-__global__ void __launch_bounds__(128, M == 2 ? kGradMinBlocks : (M == 3 ? 3 : 1)) k_le_gradient_ms(const __grid_constant__ DScene sc,
+__global__ void __launch_bounds__(128, M == 2 ? PRC_GRAD2_MINB : (M == 3 ? PRC_GRAD3_MINB : PRC_GRAD4_MINB)) k_le_gradient_ms(const __grid_constant__ DScene sc,
                                                         const __grid_constant__ VertexTable vt,
                                                         const __grid_constant__ EvalArgs ea,
                                                         double* __restrict__ own, int spread) {
@@ -395,8 +407,8 @@ __global__ void __launch_bounds__(128, M == 2 ? kGradMinBlocks : (M == 3 ? 3 : 1
                 double val[M];
 #pragma unroll
                 for (int r = 0; r < M; ++r) {
-                    double l = 0.0;
-                    v[r] = S[r].alive ? dda_step_len(S[r], nx, ny, nz, l) : -1;
+                    double l;
+                    v[r] = dda_step_packed(S[r], l);
                     val[r] = cf[r] * l;
                 }
 #pragma unroll

@@ -119,7 +119,8 @@ def test_sort_empty_store_rejected(ctx):
 
 # ---------------------------------------------------------------- K4/K5 on identical stores
 MAPPINGS = {"wavefront": dict(mode=0, packet=1), "wavefront_p2": dict(mode=0, packet=2),
-            "wavefront_p4": dict(mode=0, packet=4), "per_path": dict(mode=1, packet=1)}
+            "wavefront_p3": dict(mode=0, packet=3), "wavefront_p4": dict(mode=0, packet=4),
+            "per_path": dict(mode=1, packet=1)}
 
 
 @pytest.fixture(params=list(MAPPINGS))
@@ -129,7 +130,7 @@ def mode(ctx, request):
         ctx.set_option(k, v)
     yield request.param
     ctx.set_option("mode", 0)
-    ctx.set_option("packet", 2)
+    ctx.set_option("packet", 3)
 
 
 @pytest.mark.parametrize("name", list(FIXTURES))
