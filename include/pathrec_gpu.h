@@ -154,7 +154,8 @@ int prc_gpu_ctx_rank(const prc_gpu_ctx* ctx, int* rank, int* world);
  * LE rays per thread walked in lockstep by the gradient kernel (default 3); "spread" =
  * Morton distance between the packets of one warp (default 64); "per_species" 1 = the
  * device-resident iteration (prc_gpu_opt_step) computes per-type gradients of every
- * species (config (c)); the optimiser still updates the unknown species. */
+ * species (config (c)); the optimiser still updates the unknown species; "pad" 0 turns
+ * off the guard-free walks over the padded voxel layout (default 1; same results). */
 int prc_gpu_ctx_set_option(prc_gpu_ctx* ctx, const char* key, int64_t value);
 
 /* Uploads (and validates, finalizes) the scene; replaces any previous scene and
@@ -305,6 +306,13 @@ int prc_gpu_debug_philox(prc_gpu_ctx* ctx, uint64_t seed, uint64_t stream, uint6
  * all rays concatenated (capacity `cap`). */
 int prc_gpu_debug_walk(prc_gpu_ctx* ctx, uint64_t n, const double* rays, uint32_t* counts_out,
                        uint32_t* voxels_out, double* lengths_out, uint64_t cap);
+/* The guard-free walk the wavefront kernels use on the padded voxel layout (one border
+ * voxel per face; voxels_out are padded indices (ix+1) + (nx+2)((iy+1) + (ny+2)(iz+1))).
+ * Its spans are the reference walk's spans plus at most three trailing spans in border
+ * voxels of total length ~1e-13 |t|.  PRC_ERR_CONFIG when the scene fails the padded
+ * walk's preconditions. */
+int prc_gpu_debug_walk_padded(prc_gpu_ctx* ctx, uint64_t n, const double* rays, uint32_t* counts_out,
+                              uint32_t* voxels_out, double* lengths_out, uint64_t cap);
 /* Device Detector::pixel_of (scene.cpp:16-28) for n points against detector det. */
 int prc_gpu_debug_pixel_of(prc_gpu_ctx* ctx, int det, uint64_t n, const double* points,
                            int32_t* out);

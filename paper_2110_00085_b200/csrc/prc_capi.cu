@@ -9,6 +9,7 @@
 // (pathstore.cpp:410-516), C-ABI conventions (capi.cpp:17-32).
 #include <nccl.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -109,6 +110,7 @@ struct prc_gpu_ctx {
     int spread = 64;     // K5b lane spreading factor (packet 2: 8 best at 1e7, 64-128 at 1e8)
     int opt_per_species = 0;  // opt_step computes per-type gradients of every species
     int packet = 3;      // K5b rays per thread walked in lockstep (measured best: 3)
+    bool pad_ok = false, pad_enable = true;  // guard-free padded walks valid / allowed
     // scene
     bool have_scene = false;
     DScene dsc{};
@@ -118,7 +120,8 @@ struct prc_gpu_ctx {
     std::vector<prc_surface_desc> surfaces;
     double scene_kappa = 0.0, scene_gamma = 0.0;
     // evaluation scratch
-    DBuf<float> sp_t, bt_tot, dbeta;
+    DBuf<float> sp_t, bt_tot, dbeta, bt_pad, db_pad;  // *_pad: padded layout (pad_walk)
+    DBuf<double> g_pad;
     DBuf<double> param_beta, species_t, trace_sp, images, weights, g_span, g_vert, g_out, phong,
         g_phong, loss;
     DBuf<unsigned long long> clamps, u64tmp_a, u64tmp_b, n_trunc;
@@ -371,6 +374,19 @@ void upload_scene(prc_gpu_ctx* c, const prc_scene_desc* d) {
         off += (long long)q.rows * q.cols;
     }
     s.n_pix = off;
+    // Guard-free walks over the padded layout (prc_device.cuh, dda_walk_pad): exact when
+    // the rounding of the tmax sums (~512 ulp of a distance <= 4R) stays far below a voxel.
+    if (s.has_medium) {
+        double R = 0.0, vmin = std::min(s.vs[0], std::min(s.vs[1], s.vs[2]));
+        for (int a = 0; a < 3; ++a)
+            R = std::max({R, std::fabs(s.bmin[a]), std::fabs(s.bmax[a]), std::fabs(s.gorg[a]), std::fabs(s.gmax[a]),
+                          std::fabs(s.light_pos[a])});
+        const long long vpad = (long long)(s.dims[0] + 2) * (s.dims[1] + 2) * (s.dims[2] + 2);
+        c->pad_ok = vpad < (1ll << 31) && vmin > 0.0 && 4.0 * R < 1e9 * vmin;
+        s.pad_walk = c->pad_ok && c->pad_enable ? 1 : 0;
+        s.pnx = s.dims[0] + 2;
+        s.pnxny = (s.dims[0] + 2) * (s.dims[1] + 2);
+    }
     c->dsc = s;
     c->V = V;
     c->n_pix = off;
@@ -390,6 +406,14 @@ void upload_scene(prc_gpu_ctx* c, const prc_scene_desc* d) {
     c->images.alloc((size_t)off);
     c->weights.alloc((size_t)off);
     c->g_span.alloc((size_t)std::max<long long>(V, 1));
+    {
+        const size_t vpad = c->pad_ok ? (size_t)s.pnxny * (size_t)(s.dims[2] + 2) : 1;
+        c->bt_pad.alloc(vpad);
+        c->db_pad.alloc(vpad);
+        c->g_pad.alloc(vpad);
+        CK(cudaMemset(c->bt_pad.p, 0, c->bt_pad.bytes()));  // borders stay zero
+        CK(cudaMemset(c->db_pad.p, 0, c->db_pad.bytes()));
+    }
     c->g_vert.alloc(nsV);
     c->g_out.alloc(nsV);
     c->phong.alloc(2);
@@ -550,6 +574,9 @@ EvalArgs eval_args(prc_gpu_ctx* c, prc_gpu_store* st, const EvalRun& er, const d
     ea.clamps = c->clamps.p;
     ea.weights = er.weights;
     ea.g_span = c->g_span.p;
+    ea.bt_pad = c->bt_pad.p;
+    ea.db_pad = c->db_pad.p;
+    ea.g_pad = c->g_pad.p;
     ea.g_vert = c->g_vert.p;
     ea.g_phong = c->g_phong.p;
     ea.per_species = er.per_species ? 1 : 0;
@@ -567,6 +594,8 @@ void run_forward(prc_gpu_ctx* c, prc_gpu_store* st, const Resolved& r, const Eva
     CK(cudaEventRecord(c->ev[0], q));
     CK(launch_prep(s.n_species, c->V, r.src, st->br_tot64.p, c->sp_t.p, c->bt_tot.p, c->dbeta.p, q,
                    &c->launches));
+    if (c->mode == 0 && s.pad_walk)
+        CK(launch_pad_tables(s, c->bt_tot.p, c->dbeta.p, c->bt_pad.p, c->db_pad.p, q, &c->launches));
     if (!phong_dev) {
         const double ph[2] = {r.kappa, r.gamma};
         CK(cudaMemcpyAsync(c->phong.p, ph, sizeof ph, cudaMemcpyHostToDevice, q));
@@ -606,11 +635,13 @@ void run_gradient(prc_gpu_ctx* c, prc_gpu_store* st, const EvalArgs& ea) {
     CK(cudaMemsetAsync(c->g_vert.p, 0, c->g_vert.bytes(), q));
     CK(cudaMemsetAsync(c->g_phong.p, 0, 2 * sizeof(double), q));
     if (c->mode == 0) {
-        CK(launch_le_gradient(s, vertex_table(st), ea, st->own.p, c->spread, s.dda_packed ? c->packet : 1, q,
+        if (s.pad_walk) CK(cudaMemsetAsync(c->g_pad.p, 0, c->g_pad.bytes(), q));
+        CK(launch_le_gradient(s, vertex_table(st), ea, st->own.p, c->spread, s.pad_walk ? c->packet : 1, q,
                               &c->launches));
         CK(cudaEventRecord(c->ev[7], q));
         c->timed_grad = true;
         CK(launch_path_gradient(s, st->view(), ea, st->own.p, q, &c->launches));
+        if (s.pad_walk) CK(launch_unpad_add(s, c->g_pad.p, c->g_span.p, q, &c->launches));
     } else {
         CK(launch_gradient(s, st->view(), ea, q, &c->launches));
     }
@@ -1288,9 +1319,13 @@ PRC_EXPORT int prc_gpu_ctx_set_option(prc_gpu_ctx* ctx, const char* key, int64_t
     } else if (k == "packet") {
         if (value < 1 || value > 4) return fail(PRC_ERR_CONFIG, "packet must be in 1..4");
         ctx->packet = (int)value;
+    } else if (k == "pad") {
+        ctx->pad_enable = value != 0;
+        ctx->dsc.pad_walk = ctx->pad_ok && ctx->pad_enable ? 1 : 0;
     } else {
         return fail(PRC_ERR_CONFIG, "unknown option " + k);
     }
+    ++ctx->fwd_gen;  // a cached forward was computed under the old options
     return PRC_OK;
 }
 
@@ -1754,21 +1789,21 @@ PRC_EXPORT int prc_gpu_debug_philox(prc_gpu_ctx* ctx, uint64_t seed, uint64_t st
     ABI_CATCH
 }
 
-PRC_EXPORT int prc_gpu_debug_walk(prc_gpu_ctx* ctx, uint64_t n, const double* rays,
-                                  uint32_t* counts_out, uint32_t* voxels_out, double* lengths_out,
-                                  uint64_t cap) {
+static int debug_walk(prc_gpu_ctx* ctx, uint64_t n, const double* rays, uint32_t* counts_out,
+                      uint32_t* voxels_out, double* lengths_out, uint64_t cap, bool pad) {
     if (!ctx || !rays || !counts_out) return fail(PRC_ERR_INVALID, "null argument");
     ABI_TRY
     begin(ctx);
     ctx->check_scene();
     if (!ctx->dsc.has_medium) throw Err(PRC_ERR_CONFIG, "scene has no medium grid");
+    if (pad && !ctx->pad_ok) throw Err(PRC_ERR_CONFIG, "padded walks are not valid for this scene");
     cudaStream_t q = ctx->stream;
     DBuf<double> dr;
     DBuf<uint32_t> dc;
     dr.alloc(std::max<uint64_t>(7 * n, 1));
     dc.alloc(std::max<uint64_t>(n, 1));
     if (n) CK(cudaMemcpyAsync(dr.p, rays, 7 * n * 8, cudaMemcpyHostToDevice, q));
-    CK(launch_walk(ctx->dsc, dr.p, (long long)n, dc.p, nullptr, nullptr, nullptr, q, &ctx->launches));
+    CK(launch_walk(ctx->dsc, dr.p, (long long)n, dc.p, nullptr, nullptr, nullptr, q, &ctx->launches, pad));
     if (n) CK(cudaMemcpyAsync(counts_out, dc.p, n * 4, cudaMemcpyDeviceToHost, q));
     ctx->sync();
     if (voxels_out && lengths_out) {
@@ -1782,7 +1817,7 @@ PRC_EXPORT int prc_gpu_debug_walk(prc_gpu_ctx* ctx, uint64_t n, const double* ra
         dv.alloc(std::max<unsigned long long>(off[n], 1));
         dl.alloc(std::max<unsigned long long>(off[n], 1));
         if (n) CK(cudaMemcpyAsync(doff.p, off.data(), n * 8, cudaMemcpyHostToDevice, q));
-        CK(launch_walk(ctx->dsc, dr.p, (long long)n, dc.p, doff.p, dv.p, dl.p, q, &ctx->launches));
+        CK(launch_walk(ctx->dsc, dr.p, (long long)n, dc.p, doff.p, dv.p, dl.p, q, &ctx->launches, pad));
         if (off[n]) {
             CK(cudaMemcpyAsync(voxels_out, dv.p, off[n] * 4, cudaMemcpyDeviceToHost, q));
             CK(cudaMemcpyAsync(lengths_out, dl.p, off[n] * 8, cudaMemcpyDeviceToHost, q));
@@ -1790,6 +1825,16 @@ PRC_EXPORT int prc_gpu_debug_walk(prc_gpu_ctx* ctx, uint64_t n, const double* ra
         ctx->sync();
     }
     ABI_CATCH
+}
+
+PRC_EXPORT int prc_gpu_debug_walk(prc_gpu_ctx* ctx, uint64_t n, const double* rays, uint32_t* counts_out,
+                                  uint32_t* voxels_out, double* lengths_out, uint64_t cap) {
+    return debug_walk(ctx, n, rays, counts_out, voxels_out, lengths_out, cap, false);
+}
+
+PRC_EXPORT int prc_gpu_debug_walk_padded(prc_gpu_ctx* ctx, uint64_t n, const double* rays, uint32_t* counts_out,
+                                         uint32_t* voxels_out, double* lengths_out, uint64_t cap) {
+    return debug_walk(ctx, n, rays, counts_out, voxels_out, lengths_out, cap, true);
 }
 
 PRC_EXPORT int prc_gpu_debug_pixel_of(prc_gpu_ctx* ctx, int det, uint64_t n, const double* pts,

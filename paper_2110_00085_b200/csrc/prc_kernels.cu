@@ -602,6 +602,7 @@ __global__ void k_philox(unsigned long long seed, unsigned long long stream, uns
     for (unsigned long long i = 0; i < n; ++i) out[i] = r.u32();
 }
 
+template <bool PAD>
 __global__ void k_walk(const __grid_constant__ DScene sc, const double* rays, long long n,
                        uint32_t* counts, const unsigned long long* off, uint32_t* vox,
                        double* len) {
@@ -610,7 +611,7 @@ __global__ void k_walk(const __grid_constant__ DScene sc, const double* rays, lo
     const double* r = rays + 7 * i;
     uint32_t c = 0;
     unsigned long long w = off ? off[i] : 0;
-    dda_walk(sc, mk(r[0], r[1], r[2]), mk(r[3], r[4], r[5]), r[6], [&](int v, double ta, double tb) {
+    auto f = [&](int v, double ta, double tb) {
         if (off) {
             vox[w] = (uint32_t)v;
             len[w] = tb - ta;
@@ -618,7 +619,11 @@ __global__ void k_walk(const __grid_constant__ DScene sc, const double* rays, lo
         }
         ++c;
         return true;
-    });
+    };
+    if (PAD)
+        dda_walk_pad(sc, mk(r[0], r[1], r[2]), mk(r[3], r[4], r[5]), r[6], f);
+    else
+        dda_walk(sc, mk(r[0], r[1], r[2]), mk(r[3], r[4], r[5]), r[6], f);
     if (!off) counts[i] = c;
 }
 
@@ -910,9 +915,12 @@ cudaError_t launch_philox(unsigned long long seed, unsigned long long stream, un
 
 cudaError_t launch_walk(const DScene& sc, const double* rays, long long n, uint32_t* counts,
                         const unsigned long long* off, uint32_t* vox, double* len, cudaStream_t s,
-                        unsigned long long* launches) {
+                        unsigned long long* launches, bool pad) {
     if (n == 0) return cudaSuccess;
-    k_walk<<<grid_for(n), kTPB, 0, s>>>(sc, rays, n, counts, off, vox, len);
+    if (pad)
+        k_walk<true><<<grid_for(n), kTPB, 0, s>>>(sc, rays, n, counts, off, vox, len);
+    else
+        k_walk<false><<<grid_for(n), kTPB, 0, s>>>(sc, rays, n, counts, off, vox, len);
     LAUNCH_DONE();
 }
 

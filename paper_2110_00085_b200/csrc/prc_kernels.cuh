@@ -60,6 +60,11 @@ struct EvalArgs {
     double* g_span;         // V: transmittance part of dL/dbeta, shared by all species
     double* g_vert;         // n_vert_out x V: vertex score parts
     double* g_phong;        // [d kappa, d gamma]
+    // padded layout (DScene::pad_walk): bt_tot / dbeta with a zero border, and the
+    // padded accumulator of the LE + path span gradient (folded into g_span by k_unpad_add)
+    const float* bt_pad;
+    const float* db_pad;
+    double* g_pad;
     int per_species, legacy, do_beta;
 };
 
@@ -76,6 +81,12 @@ struct TraceArgs {
 };
 
 // ---- launchers (return cudaError_t); `launches` counts kernels issued -------------
+// Padded layout: bt_pad/db_pad interiors <- bt_tot/dbeta (borders stay zero), and
+// g_span += interior of g_pad.
+cudaError_t launch_pad_tables(const DScene& sc, const float* bt_tot, const float* dbeta, float* bt_pad,
+                              float* db_pad, cudaStream_t s, unsigned long long* launches);
+cudaError_t launch_unpad_add(const DScene& sc, const double* g_pad, double* g_span, cudaStream_t s,
+                             unsigned long long* launches);
 cudaError_t launch_trace(const DScene& sc, const TraceArgs& a, bool write, cudaStream_t s,
                          unsigned long long* launches);
 cudaError_t launch_prep(int n_species, long long V, const double* const* src_t,
@@ -175,7 +186,7 @@ cudaError_t launch_philox(unsigned long long seed, unsigned long long stream,
                           unsigned long long* launches);
 cudaError_t launch_walk(const DScene& sc, const double* rays, long long n, uint32_t* counts,
                         const unsigned long long* offsets, uint32_t* vox, double* len,
-                        cudaStream_t s, unsigned long long* launches);
+                        cudaStream_t s, unsigned long long* launches, bool pad = false);
 cudaError_t launch_pixel_of(const DScene& sc, int det, const double* pts, long long n,
                             int32_t* out, cudaStream_t s, unsigned long long* launches);
 // Per (interaction vertex, detector) event materialisation: valid, pixel, cos_le,

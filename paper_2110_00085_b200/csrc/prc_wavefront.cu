@@ -134,13 +134,9 @@ __global__ void __launch_bounds__(kTPB) k_prefix(const __grid_constant__ DScene 
             continue;
         }
         if (sc.has_medium) {
-            double diff = 0.0;
-            const float* db = ea.dbeta;
-            dda_walk(sc, xprev, mk(st.dx[r], st.dy[r], st.dz[r]), st.tt[r], [&](int v, double ta, double tb) {
-                diff = fma((double)__ldg(db + v), tb - ta, diff);
-                return true;
-            });
-            l -= diff;
+            const V3 d = mk(st.dx[r], st.dy[r], st.dz[r]);
+            l -= sc.pad_walk ? dda_optical_depth_pad(sc, xprev, d, st.tt[r], ea.db_pad)
+                             : dda_optical_depth(sc, xprev, d, st.tt[r], ea.dbeta);
         }
         lp[iv] = l;
         const uint32_t m = st.meta[r];
@@ -209,7 +205,8 @@ __global__ void __launch_bounds__(kWF, kFwdMinBlocks) k_le_forward(const __grid_
                 }
                 if (logval != -INFINITY) {
                     if (sc.has_medium) {
-                        logval -= dda_optical_depth(sc, x, w, r, ea.bt_tot);
+                        logval -= sc.pad_walk ? dda_optical_depth_pad(sc, x, w, r, ea.bt_pad)
+                                              : dda_optical_depth(sc, x, w, r, ea.bt_tot);
                     }
                     if (logval > PRC_LOG_CLAMP || logval < -PRC_LOG_CLAMP) {
                         logval = clampd(logval, -PRC_LOG_CLAMP, PRC_LOG_CLAMP);
@@ -369,7 +366,7 @@ __global__ void __launch_bounds__(128, M == 2 ? PRC_GRAD2_MINB : (M == 3 ? PRC_G
             double rr, geom, cos_le;
             event_geometry(sc, sc.det[k], x, d, kind, surf, wd, rr, geom, cos_le);
             if (ea.do_beta) {
-                S[r].init(sc, x, wd, rr);
+                S[r].init<true>(sc, x, wd, rr);  // packets run on the padded layout only
                 cf[r] = -w;
                 if (kind == VK_VOLUME) {
                     const int vox = vt.vox[i];
@@ -386,13 +383,12 @@ __global__ void __launch_bounds__(128, M == 2 ? PRC_GRAD2_MINB : (M == 3 ? PRC_G
             if (sc.target >= 0 && kind == VK_SURFACE && surf == sc.target)
                 phong_scores(ea.phong, cos_le, w, gk, gg);
         }
-        const int nx = sc.dims[0], ny = sc.dims[1], nz = sc.dims[2];
-        double* g = ea.g_span;
+        double* g = ea.g_pad;
         if (M == 2) {  // hand-scheduled pair
-            while (S[0].alive || S[1].alive) {  // packets are only used on packed grids
+            while (S[0].alive || S[1].alive) {
                 double l0, l1;
-                const int v0 = dda_step_packed(S[0], l0);
-                const int v1 = dda_step_packed(S[1], l1);
+                const int v0 = dda_step_pad(S[0], l0);
+                const int v1 = dda_step_pad(S[1], l1);
                 const double x1 = cf[1] * l1;
                 const bool same = v0 >= 0 && v0 == v1;
                 if (v0 >= 0) atomicAdd(g + v0, cf[0] * l0 + (same ? x1 : 0.0));
@@ -408,7 +404,7 @@ __global__ void __launch_bounds__(128, M == 2 ? PRC_GRAD2_MINB : (M == 3 ? PRC_G
 #pragma unroll
                 for (int r = 0; r < M; ++r) {
                     double l;
-                    v[r] = dda_step_packed(S[r], l);
+                    v[r] = dda_step_pad(S[r], l);
                     val[r] = cf[r] * l;
                 }
 #pragma unroll
@@ -459,7 +455,7 @@ __global__ void __launch_bounds__(128, M == 2 ? PRC_GRAD2_MINB : (M == 3 ? PRC_G
 // set up their next segment together (work regeneration; set-up cost is paid in batches).
 // from_here = W - prefix (suffix sums of pathstore.cpp:219-237 from own[iv]) weights the
 // incoming segment's spans; continuation score terms use after = W - prefix_next.
-template <bool PACKED>
+template <bool PAD>
 __global__ void __launch_bounds__(kTPB) k_path_gradient(const __grid_constant__ DScene sc,
                                                         const __grid_constant__ StoreView st,
                                                         const __grid_constant__ EvalArgs ea,
@@ -486,7 +482,7 @@ __global__ void __launch_bounds__(kTPB) k_path_gradient(const __grid_constant__ 
     double prefix = 0.0, cf = 0.0, gk = 0.0, gg = 0.0;
     DdaState S{};  // dead until the first segment is set up
     const int nx = sc.dims[0], ny = sc.dims[1], nz = sc.dims[2];
-    double* g = ea.g_span;
+    double* g = PAD ? ea.g_pad : ea.g_span;
     for (;;) {
         while (!done && !S.alive) {
             if (b >= B) {
@@ -506,7 +502,7 @@ __global__ void __launch_bounds__(kTPB) k_path_gradient(const __grid_constant__ 
                     phong_scores(ea.phong, st.ct[r], after, gk, gg);
             }
             if (from_here != 0.0 && ea.do_beta) {
-                S.init(sc, xprev, mk(st.dx[r], st.dy[r], st.dz[r]), st.tt[r]);
+                S.init<PAD>(sc, xprev, mk(st.dx[r], st.dy[r], st.dz[r]), st.tt[r]);
                 cf = -from_here;
             }
             prefix = prefix_next;
@@ -520,8 +516,7 @@ __global__ void __launch_bounds__(kTPB) k_path_gradient(const __grid_constant__ 
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 double len;
-                const int v = PACKED ? dda_step_packed(S, len)
-                                     : (S.alive ? dda_step_len<false>(S, nx, ny, nz, len) : -1);
+                const int v = PAD ? dda_step_pad(S, len) : (S.alive ? dda_step_len<false>(S, nx, ny, nz, len) : -1);
                 if (v >= 0) atomicAdd(g + v, cf * len);
             }
         } while (warp_count(S.alive) >= target && target > 0);
@@ -536,6 +531,28 @@ __global__ void __launch_bounds__(kTPB) k_path_gradient(const __grid_constant__ 
             atomicAdd(ea.g_phong + 1, gg);
         }
     }
+}
+
+// ------------------------------------------------------------------ padded layout
+__global__ void k_pad_tables(const __grid_constant__ DScene sc, const float* __restrict__ bt,
+                             const float* __restrict__ db, float* __restrict__ bt_pad, float* __restrict__ db_pad) {
+    const long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= sc.V) return;
+    const int nx = sc.dims[0], ny = sc.dims[1];
+    const int ix = (int)(v % nx), iy = (int)((v / nx) % ny), iz = (int)(v / ((long long)nx * ny));
+    const long long pv = (ix + 1) + (long long)sc.pnx * (iy + 1) + (long long)sc.pnxny * (iz + 1);
+    bt_pad[pv] = bt[v];
+    db_pad[pv] = db[v];
+}
+
+__global__ void k_unpad_add(const __grid_constant__ DScene sc, const double* __restrict__ g_pad,
+                            double* __restrict__ g_span) {
+    const long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= sc.V) return;
+    const int nx = sc.dims[0], ny = sc.dims[1];
+    const int ix = (int)(v % nx), iy = (int)((v / nx) % ny), iz = (int)(v / ((long long)nx * ny));
+    const long long pv = (ix + 1) + (long long)sc.pnx * (iy + 1) + (long long)sc.pnxny * (iz + 1);
+    g_span[v] += g_pad[pv];
 }
 
 }  // namespace
@@ -614,9 +631,23 @@ cudaError_t launch_le_gradient(const DScene& sc, const VertexTable& vt, const Ev
 cudaError_t launch_path_gradient(const DScene& sc, const StoreView& st, const EvalArgs& ea,
                                  const double* own, cudaStream_t s, unsigned long long* launches) {
     if (st.n == 0) return cudaSuccess;
-    if (sc.dda_packed)
+    if (sc.pad_walk)
         k_path_gradient<true><<<grid_for((long long)st.n, kTPB), kTPB, 0, s>>>(sc, st, ea, own);
     else
         k_path_gradient<false><<<grid_for((long long)st.n, kTPB), kTPB, 0, s>>>(sc, st, ea, own);
+    LAUNCH_DONE();
+}
+
+cudaError_t launch_pad_tables(const DScene& sc, const float* bt_tot, const float* dbeta, float* bt_pad,
+                              float* db_pad, cudaStream_t s, unsigned long long* launches) {
+    if (sc.V == 0) return cudaSuccess;
+    k_pad_tables<<<grid_for(sc.V, 256), 256, 0, s>>>(sc, bt_tot, dbeta, bt_pad, db_pad);
+    LAUNCH_DONE();
+}
+
+cudaError_t launch_unpad_add(const DScene& sc, const double* g_pad, double* g_span, cudaStream_t s,
+                             unsigned long long* launches) {
+    if (sc.V == 0) return cudaSuccess;
+    k_unpad_add<<<grid_for(sc.V, 256), 256, 0, s>>>(sc, g_pad, g_span);
     LAUNCH_DONE();
 }

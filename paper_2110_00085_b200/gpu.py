@@ -113,6 +113,7 @@ def load_library(path: Optional[str] = None):
         "prc_gpu_store_stats": [vp, vp, _u64p],
         "prc_gpu_debug_philox": [vp, C.c_uint64, C.c_uint64, C.c_uint64, _u32p],
         "prc_gpu_debug_walk": [vp, C.c_uint64, _dp, _u32p, _u32p, _dp, C.c_uint64],
+        "prc_gpu_debug_walk_padded": [vp, C.c_uint64, _dp, _u32p, _u32p, _dp, C.c_uint64],
         "prc_gpu_debug_pixel_of": [vp, C.c_int, C.c_uint64, _dp, _i32p],
     }
     for name, args in sig.items():
@@ -420,17 +421,18 @@ class Context:
         _check(_lib.prc_gpu_debug_philox(self.ptr, seed, stream, n, _ptr(out, _u32p)))
         return out
 
-    def debug_walk(self, rays: np.ndarray):
+    def debug_walk(self, rays: np.ndarray, padded: bool = False):
+        """Device DDA spans of n rays (n x 7); padded=True: the guard-free walk over the
+        padded layout (voxel ids are padded indices)."""
+        fn = _lib.prc_gpu_debug_walk_padded if padded else _lib.prc_gpu_debug_walk
         rays = np.ascontiguousarray(rays, dtype=np.float64).reshape(-1, 7)
         n = rays.shape[0]
         counts = np.zeros(n, np.uint32)
-        _check(_lib.prc_gpu_debug_walk(self.ptr, n, _ptr(rays, _dp), _ptr(counts, _u32p), None,
-                                       None, 0))
+        _check(fn(self.ptr, n, _ptr(rays, _dp), _ptr(counts, _u32p), None, None, 0))
         tot = int(counts.sum())
         vox = np.zeros(max(tot, 1), np.uint32)
         ln = np.zeros(max(tot, 1))
-        _check(_lib.prc_gpu_debug_walk(self.ptr, n, _ptr(rays, _dp), _ptr(counts, _u32p),
-                                       _ptr(vox, _u32p), _ptr(ln, _dp), tot))
+        _check(fn(self.ptr, n, _ptr(rays, _dp), _ptr(counts, _u32p), _ptr(vox, _u32p), _ptr(ln, _dp), tot))
         return counts, vox[:tot], ln[:tot]
 
     def debug_pixel_of(self, det: int, pts: np.ndarray) -> np.ndarray:

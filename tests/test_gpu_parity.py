@@ -75,6 +75,93 @@ def test_device_dda_bit_exact(ctx, port, name):
     assert np.array_equal(l1.view(np.uint64), l2.view(np.uint64))
 
 
+def _adversarial_rays(lo, hi, n_vox, rng, n=4000):
+    """Rays that stress the end of a walk: exits through grid corners and edges (tmax ties
+    on two or three axes), axis-aligned rays on voxel boundaries, rays entering from
+    outside, grazing rays on a face, and random rays."""
+    lo, hi = np.asarray(lo, float), np.asarray(hi, float)
+    vs = (hi - lo) / np.asarray(n_vox)
+    out = []
+    x = lo + rng.uniform(0.02, 0.98, size=(n, 3)) * (hi - lo)
+    corners = lo + (hi - lo) * rng.integers(0, 2, size=(n, 3))
+    edges = corners.copy()
+    ax = rng.integers(0, 3, size=n)
+    edges[np.arange(n), ax] = lo[ax] + vs[ax] * rng.integers(0, np.asarray(n_vox)[ax])
+    for tgt in (corners, edges):
+        d = tgt - x
+        r = np.linalg.norm(d, axis=1)
+        out.append(np.c_[x, d / r[:, None], r * rng.choice([1.0, 2.0], size=n)])
+    for a in range(3):  # axis-aligned, origins on voxel boundaries
+        o = lo + vs * rng.integers(0, np.asarray(n_vox), size=(n, 3)) + vs * 0.5 * rng.integers(0, 2, size=(n, 3))
+        d = np.zeros((n, 3))
+        d[:, a] = rng.choice([-1.0, 1.0], size=n)
+        out.append(np.c_[o, d, np.full(n, 3.0 * (hi - lo).max())])
+    o = lo - 0.5 * (hi - lo) + rng.uniform(0, 2, size=(n, 3)) * (hi - lo)  # from outside
+    d = x - o
+    d /= np.linalg.norm(d, axis=1)[:, None]
+    out.append(np.c_[o, d, np.full(n, 4.0 * (hi - lo).max())])
+    o = x.copy()  # grazing: on the z = lo face, moving within it
+    o[:, 2] = lo[2]
+    d = rng.normal(size=(n, 3))
+    d[:, 2] = 0.0
+    d /= np.linalg.norm(d, axis=1)[:, None]
+    out.append(np.c_[o, d, np.full(n, 2.0 * (hi - lo).max())])
+    return np.concatenate(out)
+
+
+@pytest.mark.parametrize("name", ["tomo2", "cloud", "mixed", "bench"])
+def test_padded_walk_is_reference_walk_plus_border_tail(ctx, port, name):
+    """The guard-free walk of the wavefront kernels (prc_device.cuh dda_walk_pad) emits
+    exactly the reference's spans (voxel and length bits), followed by at most three
+    spans in border voxels of the padded layout with negligible total length."""
+    scene = S.cloud_scene(128, 16, 16) if name == "bench" else FIXTURES[name]["scene"]()
+    ctx.upload(scene)
+    g = scene.grid
+    nx, ny, nz = g.dims
+    lo = np.asarray(g.origin, float)
+    hi = lo + np.asarray(g.voxel_size) * np.asarray(g.dims)
+    rays = _adversarial_rays(lo, hi, g.dims, np.random.default_rng(17))
+    c1, v1, l1 = ctx.debug_walk(rays, padded=True)
+    c2, v2, l2 = port.walk(scene, rays)
+    o1 = np.r_[0, np.cumsum(c1.astype(np.int64))]
+    o2 = np.r_[0, np.cumsum(c2.astype(np.int64))]
+    extra = c1.astype(np.int64) - c2.astype(np.int64)
+    assert extra.min() >= 0 and extra.max() <= 3
+    pnx, pny = nx + 2, ny + 2
+    pv = v1.astype(np.int64)
+    px, py, pz = pv % pnx, (pv // pnx) % pny, pv // (pnx * pny)
+    border = (px == 0) | (px == nx + 1) | (py == 0) | (py == ny + 1) | (pz == 0) | (pz == nz + 1)
+    interior = (px - 1) + nx * ((py - 1) + ny * (pz - 1))
+    head = np.concatenate([np.arange(o1[i], o1[i] + c2[i]) for i in range(len(c2))]) if len(c2) else []
+    head = np.asarray(head, np.int64)
+    assert np.array_equal(interior[head], v2.astype(np.int64))
+    assert not border[head].any()
+    assert np.array_equal(l1[head].view(np.uint64), l2.view(np.uint64))
+    tail = np.setdiff1d(np.arange(len(v1)), head)
+    assert border[tail].all()
+    scale = np.abs(rays[:, :3]).max() + np.abs(rays[:, 6]).max()
+    assert (l1[tail] <= 1e-12 * scale).all()
+    print(f"{name}: {len(rays)} rays, {int((extra > 0).sum())} walks end with a border tail "
+          f"(max tail length {l1[tail].max() if len(tail) else 0.0:.2e})")
+
+
+def test_pad_option_same_results(ctx, golden_dir):
+    """Padded guard-free walks on/off: identical images (the border beta is zero) and
+    gradients equal up to fp64 atomic ordering."""
+    scene = FIXTURES["cloud"]["scene"]()
+    ctx.upload(scene)
+    st = ctx.load_store(str(golden_dir / "cloud.pstr"))
+    ctx.sort_by_size(st)
+    w = np.linspace(-1.0, 2.0, scene.pixel_count)
+    res = []
+    for pad in (1, 0):
+        ctx.set_option("pad", pad)
+        res.append(ctx.evaluate_store(scene, st, perturbed(scene), EvalOptions(want_grad=True, pixel_weights=w)))
+    ctx.set_option("pad", 1)
+    assert img_err(res[0].images, res[1].images) <= 1e-13
+    assert grad_err(res[0].grad_beta, res[1].grad_beta) <= 1e-11
+
+
 @pytest.mark.parametrize("name", ["tomo2", "cloud", "mixed"])
 def test_device_pixel_of_bit_exact(ctx, name):
     g = golden("common")
@@ -120,7 +207,7 @@ def test_sort_empty_store_rejected(ctx):
 # ---------------------------------------------------------------- K4/K5 on identical stores
 MAPPINGS = {"wavefront": dict(mode=0, packet=1), "wavefront_p2": dict(mode=0, packet=2),
             "wavefront_p3": dict(mode=0, packet=3), "wavefront_p4": dict(mode=0, packet=4),
-            "per_path": dict(mode=1, packet=1)}
+            "wavefront_guarded": dict(mode=0, packet=3, pad=0), "per_path": dict(mode=1, packet=1)}
 
 
 @pytest.fixture(params=list(MAPPINGS))
@@ -131,6 +218,7 @@ def mode(ctx, request):
     yield request.param
     ctx.set_option("mode", 0)
     ctx.set_option("packet", 3)
+    ctx.set_option("pad", 1)
 
 
 @pytest.mark.parametrize("name", list(FIXTURES))
