@@ -40,7 +40,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str = OUT
     tag = "" if out == OUT else "." + os.path.basename(out).replace(".so", "")
     objs = []
     for s in SOURCES:
-        obj = os.path.join(SRC, s.replace(".cu", tag + ".o"))
+        obj = os.path.join(SRC if not tag else os.path.dirname(out), s.replace(".cu", tag + ".o"))
         cmd = [NVCC, *FLAGS, *("-D" + d for d in defines), "-c", os.path.join(SRC, s), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:

@@ -391,9 +391,24 @@ __global__ void __launch_bounds__(128, M == 2 ? PRC_GRAD2_MINB : (M == 3 ? PRC_G
                 const int v1 = dda_step_pad(S[1], l1);
                 const double x1 = cf[1] * l1;
                 const bool same = v0 >= 0 && v0 == v1;
-                if (v0 >= 0) atomicAdd(g + v0, cf[0] * l0 + (same ? x1 : 0.0));
-                if (v1 >= 0 && !same) atomicAdd(g + v1, x1);
+                red_add_if(g, v0, cf[0] * l0 + (same ? x1 : 0.0));
+                red_add_if(g, same ? -1 : v1, x1);
             }
+        } else if (M == 3) {  // hand-scheduled triple (the default packet)
+            auto step3 = [&]() {
+                double l0, l1, l2;
+                const int v0 = dda_step_pad(S[0], l0);
+                const int v1 = dda_step_pad(S[1], l1);
+                const int v2 = dda_step_pad(S[2], l2);
+                const double x1 = cf[1] * l1, x2 = cf[2] * l2;
+                const bool s10 = v1 >= 0 && v1 == v0;
+                const bool s20 = v2 >= 0 && v2 == v0;
+                const bool s21 = v2 >= 0 && v2 == v1 && !s20;
+                red_add_if(g, v0, cf[0] * l0 + (s10 ? x1 : 0.0) + (s20 ? x2 : 0.0));
+                red_add_if(g, s10 ? -1 : v1, x1 + (s21 ? x2 : 0.0));
+                red_add_if(g, (s20 || s21) ? -1 : v2, x2);
+            };
+            while (S[0].alive || S[1].alive || S[2].alive) step3();  // (unrolling x2 measured slower)
         } else {
             bool any = false;
 #pragma unroll
@@ -422,7 +437,7 @@ __global__ void __launch_bounds__(128, M == 2 ? PRC_GRAD2_MINB : (M == 3 ? PRC_G
                 any = false;
 #pragma unroll
                 for (int r = 0; r < M; ++r) {
-                    if (v[r] >= 0) atomicAdd(g + v[r], val[r]);
+                    red_add_if(g, v[r], val[r]);
                     any |= S[r].alive;
                 }
             }
@@ -517,7 +532,7 @@ __global__ void __launch_bounds__(kTPB) k_path_gradient(const __grid_constant__ 
             for (int u = 0; u < 4; ++u) {
                 double len;
                 const int v = PAD ? dda_step_pad(S, len) : (S.alive ? dda_step_len<false>(S, nx, ny, nz, len) : -1);
-                if (v >= 0) atomicAdd(g + v, cf * len);
+                red_add_if(g, v, cf * len);
             }
         } while (warp_count(S.alive) >= target && target > 0);
     }
