@@ -26,12 +26,13 @@ namespace {
 
 constexpr int kWF = 256;  // vertices per CTA in the wavefront kernels
 constexpr int kTPB = 128;
-// Occupancy (measured on B200 at 1e8 paths, config (b)): K4b at 6 CTAs x 256 threads
-// (40 registers, spills outside the DDA loop) 604 ms vs 5 CTAs 613, 4 CTAs 639, 3 CTAs
-// 714; K5b packet-3 at 4 CTAs x 128 threads (128 registers) 937 ms vs 3 CTAs 977, 2 CTAs
-// 977, 5 CTAs 1102; packet 2 (4 CTAs) 1108, packet 4 (3 CTAs) 1132.
-#ifndef PRC_FWD_MINB  // -D overrides are for A/B builds (scripts/build_variant.sh)
-#define PRC_FWD_MINB 6
+// Occupancy (measured on B200 at 1e8 paths, config (b)).  K4b with the guarded walk: 6
+// CTAs x 256 threads (40 registers) 604 ms vs 5 CTAs 613, 4 CTAs 639, 3 CTAs 714; with
+// the padded, software-pipelined walk: 5 CTAs (48 registers) 449 ms vs 6 CTAs 458.  K5b
+// packet-3 at 4 CTAs x 128 threads (128 registers) 937 ms vs 3 CTAs 977, 2 CTAs 977, 5
+// CTAs 1102; packet 2 (4 CTAs) 1108, packet 4 (3 CTAs) 1132.
+#ifndef PRC_FWD_MINB  // -D overrides are for A/B builds (scripts/variants_lib.sh)
+#define PRC_FWD_MINB 5
 #endif
 #ifndef PRC_GRAD2_MINB
 #define PRC_GRAD2_MINB 4
