@@ -34,6 +34,9 @@ constexpr int kTPB = 128;
 #ifndef PRC_FWD_MINB  // -D overrides are for A/B builds (scripts/variants_lib.sh)
 #define PRC_FWD_MINB 5
 #endif
+#ifndef PRC_GRAD1_MINB
+#define PRC_GRAD1_MINB 3
+#endif
 #ifndef PRC_GRAD2_MINB
 #define PRC_GRAD2_MINB 4
 #endif
@@ -245,7 +248,7 @@ __device__ __forceinline__ double score_j(const DScene& sc, const EvalArgs& ea, 
 // spreading: within each chunk of 32*spread vertices, lane l of warp w takes vertex
 // l*spread + w, so one RED instruction touches 32 distinct Morton neighbourhoods instead
 // of (at high vertex density) one voxel 32 times.
-__global__ void __launch_bounds__(kWF, 3) k_le_gradient(const __grid_constant__ DScene sc,
+__global__ void __launch_bounds__(kWF, PRC_GRAD1_MINB) k_le_gradient(const __grid_constant__ DScene sc,
                                                         const __grid_constant__ VertexTable vt,
                                                         const __grid_constant__ EvalArgs ea,
                                                         double* __restrict__ own, int spread) {
@@ -285,11 +288,15 @@ __global__ void __launch_bounds__(kWF, 3) k_le_gradient(const __grid_constant__ 
         event_geometry(sc, sc.det[k], x, mk(vt.dx[i], vt.dy[i], vt.dz[i]), kind, surf, wd, r, geom, cos_le);
         if (ea.do_beta) {
             const double cf = -w;
-            double* gs = ea.g_span;
-            dda_walk(sc, x, wd, r, [&](int v, double ta, double tb) {
-                atomicAdd(gs + v, cf * (tb - ta));
-                return true;
-            });
+            if (sc.pad_walk) {
+                dda_scatter_pad(sc, x, wd, r, ea.g_pad, cf);
+            } else {
+                double* gs = ea.g_span;
+                dda_walk(sc, x, wd, r, [&](int v, double ta, double tb) {
+                    atomicAdd(gs + v, cf * (tb - ta));
+                    return true;
+                });
+            }
             if (kind == VK_VOLUME) {
                 const double num = ea.legacy ? 0.0 : scat_num(sc, ea.sp_t, vox, cos_le);
                 if (single) {
