@@ -120,8 +120,8 @@ struct prc_gpu_ctx {
     std::vector<prc_surface_desc> surfaces;
     double scene_kappa = 0.0, scene_gamma = 0.0;
     // evaluation scratch
-    DBuf<float> sp_t, bt_tot, dbeta, bt_pad, db_pad;  // *_pad: padded layout (pad_walk)
-    DBuf<double> g_pad;
+    DBuf<float> sp_t, bt_tot, dbeta;
+    DBuf<double> bt_pad, db_pad, g_pad;  // padded layout (pad_walk)
     DBuf<double> param_beta, species_t, trace_sp, images, weights, g_span, g_vert, g_out, phong,
         g_phong, loss;
     DBuf<unsigned long long> clamps, u64tmp_a, u64tmp_b, n_trunc;

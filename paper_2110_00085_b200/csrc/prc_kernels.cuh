@@ -62,8 +62,8 @@ struct EvalArgs {
     double* g_phong;        // [d kappa, d gamma]
     // padded layout (DScene::pad_walk): bt_tot / dbeta with a zero border, and the
     // padded accumulator of the LE + path span gradient (folded into g_span by k_unpad_add)
-    const float* bt_pad;
-    const float* db_pad;
+    const double* bt_pad;  // fp64: the walk's FMA takes it without an F2F conversion
+    const double* db_pad;
     double* g_pad;
     int per_species, legacy, do_beta;
 };
@@ -83,8 +83,8 @@ struct TraceArgs {
 // ---- launchers (return cudaError_t); `launches` counts kernels issued -------------
 // Padded layout: bt_pad/db_pad interiors <- bt_tot/dbeta (borders stay zero), and
 // g_span += interior of g_pad.
-cudaError_t launch_pad_tables(const DScene& sc, const float* bt_tot, const float* dbeta, float* bt_pad,
-                              float* db_pad, cudaStream_t s, unsigned long long* launches);
+cudaError_t launch_pad_tables(const DScene& sc, const float* bt_tot, const float* dbeta, double* bt_pad,
+                              double* db_pad, cudaStream_t s, unsigned long long* launches);
 cudaError_t launch_unpad_add(const DScene& sc, const double* g_pad, double* g_span, cudaStream_t s,
                              unsigned long long* launches);
 cudaError_t launch_trace(const DScene& sc, const TraceArgs& a, bool write, cudaStream_t s,

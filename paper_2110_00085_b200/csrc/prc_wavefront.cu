@@ -558,14 +558,14 @@ __global__ void __launch_bounds__(kTPB) k_path_gradient(const __grid_constant__ 
 
 // ------------------------------------------------------------------ padded layout
 __global__ void k_pad_tables(const __grid_constant__ DScene sc, const float* __restrict__ bt,
-                             const float* __restrict__ db, float* __restrict__ bt_pad, float* __restrict__ db_pad) {
+                             const float* __restrict__ db, double* __restrict__ bt_pad, double* __restrict__ db_pad) {
     const long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= sc.V) return;
     const int nx = sc.dims[0], ny = sc.dims[1];
     const int ix = (int)(v % nx), iy = (int)((v / nx) % ny), iz = (int)(v / ((long long)nx * ny));
     const long long pv = (ix + 1) + (long long)sc.pnx * (iy + 1) + (long long)sc.pnxny * (iz + 1);
-    bt_pad[pv] = bt[v];
-    db_pad[pv] = db[v];
+    bt_pad[pv] = (double)bt[v];
+    db_pad[pv] = (double)db[v];
 }
 
 __global__ void k_unpad_add(const __grid_constant__ DScene sc, const double* __restrict__ g_pad,
@@ -661,8 +661,8 @@ cudaError_t launch_path_gradient(const DScene& sc, const StoreView& st, const Ev
     LAUNCH_DONE();
 }
 
-cudaError_t launch_pad_tables(const DScene& sc, const float* bt_tot, const float* dbeta, float* bt_pad,
-                              float* db_pad, cudaStream_t s, unsigned long long* launches) {
+cudaError_t launch_pad_tables(const DScene& sc, const float* bt_tot, const float* dbeta, double* bt_pad,
+                              double* db_pad, cudaStream_t s, unsigned long long* launches) {
     if (sc.V == 0) return cudaSuccess;
     k_pad_tables<<<grid_for(sc.V, 256), 256, 0, s>>>(sc, bt_tot, dbeta, bt_pad, db_pad);
     LAUNCH_DONE();
