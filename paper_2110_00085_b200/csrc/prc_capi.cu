@@ -383,6 +383,13 @@ void upload_scene(prc_gpu_ctx* c, const prc_scene_desc* d) {
                           std::fabs(s.light_pos[a])});
         const long long vpad = (long long)(s.dims[0] + 2) * (s.dims[1] + 2) * (s.dims[2] + 2);
         c->pad_ok = vpad < (1ll << 31) && vmin > 0.0 && 4.0 * R < 1e9 * vmin;
+        s.vs_pow2 = 1;
+        for (int a = 0; a < 3; ++a) {
+            int e = 0;
+            const double m = std::frexp(s.vs[a], &e);
+            if (!(m == 0.5 && e >= -59 && e <= 21)) s.vs_pow2 = 0;
+            s.inv_vs[a] = 1.0 / s.vs[a];
+        }
         s.pad_walk = c->pad_ok && c->pad_enable ? 1 : 0;
         s.pnx = s.dims[0] + 2;
         s.pnxny = (s.dims[0] + 2) * (s.dims[1] + 2);

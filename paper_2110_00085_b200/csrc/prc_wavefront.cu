@@ -184,6 +184,9 @@ __global__ void __launch_bounds__(kWF, kFwdMinBlocks) k_le_forward(const __grid_
     const int surf = meta_surface(meta);
     const bool live = act && lpv != -INFINITY;
     const double den = (live && kind == VK_VOLUME) ? (double)ea.br_tot[vox] : 0.0;
+    // lp - log(den) is per vertex: one log per camera event instead of two (the sum is
+    // re-associated, a change of ~1e-16 relative in the event value)
+    const double lbase = den > 0.0 ? lpv - log(den) : 0.0;
     unsigned clamps = 0;
     for (int k = 0; k < sc.n_det; ++k) {
         float val = 0.0f;
@@ -202,7 +205,7 @@ __global__ void __launch_bounds__(kWF, kFwdMinBlocks) k_le_forward(const __grid_
                 double logval = -INFINITY;
                 if (kind == VK_VOLUME) {
                     const double num = scat_num(sc, ea.sp_t, vox, cos_le);
-                    if (num > 0.0 && den > 0.0) logval = lpv + log(num) - log(den);
+                    if (num > 0.0 && den > 0.0) logval = lbase + log(num);
                 } else {
                     const double fr = surf_brdf(sc, ea.phong, surf, cos_le);
                     if (fr > 0.0) logval = lpv + log(fr);
