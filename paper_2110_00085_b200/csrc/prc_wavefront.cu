@@ -28,11 +28,12 @@ constexpr int kWF = 256;  // vertices per CTA in the wavefront kernels
 constexpr int kTPB = 128;
 // Occupancy (measured on B200 at 1e8 paths, config (b)).  K4b with the guarded walk: 6
 // CTAs x 256 threads (40 registers) 604 ms vs 5 CTAs 613, 4 CTAs 639, 3 CTAs 714; with
-// the padded, software-pipelined walk: 5 CTAs (48 registers) 449 ms vs 6 CTAs 458.  K5b
+// the padded, software-pipelined walk: 5 CTAs (48 registers) 449 ms vs 6 CTAs 458; with
+// four steps per trip: 4 CTAs (64 registers) 411 ms vs 5 CTAs 430, 6 CTAs 876.  K5b
 // packet-3 at 4 CTAs x 128 threads (128 registers) 937 ms vs 3 CTAs 977, 2 CTAs 977, 5
 // CTAs 1102; packet 2 (4 CTAs) 1108, packet 4 (3 CTAs) 1132.
 #ifndef PRC_FWD_MINB  // -D overrides are for A/B builds (scripts/variants_lib.sh)
-#define PRC_FWD_MINB 5
+#define PRC_FWD_MINB 4
 #endif
 #ifndef PRC_GRAD1_MINB
 #define PRC_GRAD1_MINB 3
