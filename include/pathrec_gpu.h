@@ -20,6 +20,14 @@
  *   pathrec::save_store / load_store (PSTR v1) pathstore.cpp:410-516
  *        -> prc_gpu_store_export_pstr / prc_gpu_store_import_pstr
  *
+ * Around the loop (the Algorithm-2 driver):
+ *   reconstruct with a stage schedule          inverse.cpp:154-263, inverse.hpp:23-34
+ *        -> prc_gpu_reconstruct_schedule
+ *   space_carve / metrics / downsample_images inverse.cpp:69-133
+ *        -> prc_gpu_space_carve (device), prc_gpu_metrics, prc_gpu_downsample_images
+ *   save_grid / load_grid (VGRD v1), save_csv   io.cpp:32-76, 147-155
+ *        -> prc_gpu_save_grid / prc_gpu_load_grid, checkpoints of the schedule
+ *
  * Conventions follow the reference C ABI (include/pathrec.h:11-23, src/capi.cpp:17-32):
  * opaque handles, int error codes, a thread-local last-error string, no exceptions
  * across the boundary, caller-owned option structs, one *_free per handle.
@@ -278,6 +286,79 @@ typedef struct {
 int prc_gpu_reconstruct(prc_gpu_ctx* ctx, const prc_gpu_params* initial, const double* gt_images,
                         const prc_gpu_adam_config* adam, const prc_gpu_reconstruct_opts* opts,
                         double* loss_history, uint64_t* sampling_phases_out);
+
+/* ---------------------------------------------------------------------------
+ * The Algorithm-2 driver around the loop (inverse.cpp:69-263, io.cpp:32-76, 147-155).
+ * ------------------------------------------------------------------------- */
+
+typedef struct {              /* Stage (inverse.hpp:23-26) */
+    int rows, cols;           /* detector resolution; <= 0 keeps the current value */
+    uint64_t n_paths;
+} prc_gpu_stage;
+
+typedef struct {              /* Schedule (inverse.hpp:28-35) + ReconstructOptions (:66-76) */
+    uint64_t seed;
+    int max_bounces;          /* trace budget (RenderOptions::max_bounces, default 500) */
+    int recycle_period;       /* N_r */
+    int max_iterations;
+    const prc_gpu_stage* stages;
+    int n_stages;             /* >= 1 */
+    int saturation_window;    /* default 20 */
+    double saturation_rel_improvement;  /* default 0.01 */
+    int checkpoint_every;     /* 0 disables checkpoints */
+    const char* checkpoint_dir;         /* NULL or "" disables checkpoints */
+    int length_unit;          /* VGRD unit tag of the checkpoints (LengthUnit) */
+    const prc_gpu_params* truth;        /* optional ground-truth unknowns for eps/delta */
+} prc_gpu_schedule;
+
+typedef struct {              /* IterationLog (inverse.hpp:46-53) */
+    int iter;
+    double time_s, loss, eps, delta;
+    int stage;
+} prc_gpu_iteration_log;
+
+/* reconstruct() with a stage schedule (inverse.cpp:154-263): at every resample
+ * boundary (t % N_r == 0) a pending stage change is applied first -- every detector
+ * takes the stage's rows/cols and the ground truth is block-sum downsampled to it --
+ * then paths are traced under the iterate with the stage's n_paths (seed schedule of
+ * inverse.cpp:193) and sorted.  Each iteration logs (loss, eps/delta against `truth`),
+ * optionally checkpoints the pre-update unknowns (VGRD) and the history (CSV) to
+ * checkpoint_dir, then takes the residual-weighted gradient and the ADAM step.  A stage
+ * saturates when the relative loss improvement over saturation_window iterations falls
+ * below saturation_rel_improvement.  gt_images are at the uploaded detector resolution.
+ * The scene's detector resolution is restored on return.  history: max_iterations rows
+ * or NULL; the counters may be NULL. */
+int prc_gpu_reconstruct_schedule(prc_gpu_ctx* ctx, const prc_gpu_params* initial, const double* gt_images,
+                                 const prc_gpu_adam_config* adam, const prc_gpu_schedule* schedule,
+                                 prc_gpu_iteration_log* history, uint64_t* sampling_phases_out,
+                                 uint64_t* truncated_paths_out);
+
+/* space_carve (inverse.cpp:69-101) on the device: a voxel is occupied when its centre
+ * projects into every detector at a pixel above threshold_fraction of that view's
+ * maximum in gt_images (host, uploaded resolution).  mask_out: voxel_count bytes;
+ * beta_out: voxel_count doubles (fill_extinction where occupied, else 0); either may
+ * be NULL.  PRC_ERR_INVALID with fewer than 2 detectors or without a medium. */
+int prc_gpu_space_carve(prc_gpu_ctx* ctx, const double* gt_images, double threshold_fraction,
+                        double fill_extinction, uint8_t* mask_out, double* beta_out);
+
+/* metrics (inverse.cpp:103-114): eps = sum|t - e| / sum|t|, delta = (sum|t| - sum|e|) / sum|t|.
+ * Host arithmetic in the reference's order. */
+int prc_gpu_metrics(const double* estimate, const double* truth, uint64_t n, double* eps, double* delta);
+
+/* downsample_images (inverse.cpp:116-133): block sums of n_images images, image i of
+ * rows[i] x cols[i] (row-major, concatenated), to rows_out x cols_out each (copied when
+ * equal).  out: n_images * rows_out * cols_out doubles. */
+int prc_gpu_downsample_images(int n_images, const int* rows, const int* cols, const double* images,
+                              int rows_out, int cols_out, double* out);
+
+/* VGRD v1 (io.cpp:32-76): "VGRD", u32 1, u32 dims[3], f64 origin[3], f64 voxel_size[3],
+ * u8 unit, f32 values[prod dims].  save_grid writes values as f32; load_grid fills
+ * dims/origin/voxel_size/unit (any may be NULL) and, when values_out is non-NULL,
+ * capacity >= prod dims values (f64). */
+int prc_gpu_save_grid(const char* path, const int dims[3], const prc_vec3* origin, const prc_vec3* voxel_size,
+                      int length_unit, const double* values);
+int prc_gpu_load_grid(const char* path, int dims_out[3], prc_vec3* origin_out, prc_vec3* voxel_size_out,
+                      int* length_unit_out, double* values_out, uint64_t capacity);
 
 /* ---------------------------------------------------------------------------
  * Timing and device-side diagnostics (used by tests and bench; not on the API path).

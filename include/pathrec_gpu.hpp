@@ -21,6 +21,7 @@
 // the context's GPU (one process per GPU; see Context(device, rank, world, nccl_id)).
 #pragma once
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -483,6 +484,118 @@ inline ReconstructResult reconstruct(Context& ctx, const Scene& scene, const Ima
     check(prc_gpu_opt_params(ctx.get(), r.params.beta.empty() ? nullptr : r.params.beta.data(), &r.params.kappa_s,
                              &r.params.gamma));
     return r;
+}
+
+// inverse.hpp:23-76 / inverse.cpp:154-263: the stage-scheduled loop (coarse-to-fine
+// stages, saturation, eps/delta against a truth, VGRD + CSV checkpoints)
+struct Stage {
+    int rows = 0, cols = 0;  // <= 0 keeps the current resolution
+    uint64_t n_paths = 0;
+};
+struct Schedule {
+    int recycle_period = 30;
+    int max_iterations = 100;
+    std::vector<Stage> stages;
+    int saturation_window = 20;
+    double saturation_rel_improvement = 0.01;
+    int checkpoint_every = 0;
+};
+struct ScheduleOptions {
+    AdamConfig adam;
+    Schedule schedule;
+    uint64_t seed = 0;
+    int max_bounces = 500;
+    const ParamSet* truth = nullptr;
+    std::string checkpoint_dir;
+    int length_unit = 0;  // LengthUnit tag of the VGRD checkpoints
+};
+struct IterationLog {
+    int iter = 0;
+    double time_s = 0.0, loss = 0.0, eps = 0.0, delta = 0.0;
+    int stage = 0;
+};
+struct ScheduleResult {
+    ParamSet params;
+    std::vector<IterationLog> history;
+    uint64_t sampling_phases = 0, truncated_paths = 0;
+};
+inline ScheduleResult reconstruct(Context& ctx, const Scene& scene, const ImageSet& gt, const ParamSet& initial,
+                                  const ScheduleOptions& opt) {
+    if (opt.schedule.stages.empty()) throw std::invalid_argument("reconstruct: schedule needs at least one stage");
+    ctx.use(scene);
+    detail::ParamsC pc(initial);
+    std::vector<double> g = detail::flatten(gt);
+    prc_gpu_adam_config a{opt.adam.alpha, opt.adam.eta1, opt.adam.eta2, opt.adam.eps_guard,
+                          opt.adam.project_nonneg ? 1 : 0,
+                          opt.adam.step_scale.empty() ? nullptr : opt.adam.step_scale.data(),
+                          (int)opt.adam.step_scale.size()};
+    std::vector<prc_gpu_stage> st;
+    for (const auto& x : opt.schedule.stages) st.push_back({x.rows, x.cols, x.n_paths});
+    std::unique_ptr<detail::ParamsC> tc;
+    if (opt.truth) tc.reset(new detail::ParamsC(*opt.truth));
+    prc_gpu_schedule sch{opt.seed, opt.max_bounces, opt.schedule.recycle_period, opt.schedule.max_iterations,
+                         st.data(), (int)st.size(), opt.schedule.saturation_window,
+                         opt.schedule.saturation_rel_improvement, opt.schedule.checkpoint_every,
+                         opt.checkpoint_dir.empty() ? nullptr : opt.checkpoint_dir.c_str(), opt.length_unit,
+                         tc ? &tc->p : nullptr};
+    std::vector<prc_gpu_iteration_log> h((size_t)std::max(1, opt.schedule.max_iterations));
+    ScheduleResult r;
+    check(prc_gpu_reconstruct_schedule(ctx.get(), &pc.p, g.data(), &a, &sch, h.data(), &r.sampling_phases,
+                                       &r.truncated_paths));
+    for (int t = 0; t < opt.schedule.max_iterations; ++t)
+        r.history.push_back({h[t].iter, h[t].time_s, h[t].loss, h[t].eps, h[t].delta, h[t].stage});
+    const size_t V = scene.species.empty() ? 0 : (size_t)scene.species[0].extinction.geom.voxel_count();
+    if (scene.unknown_species() >= 0) r.params.beta.assign(V, 0.0);
+    check(prc_gpu_opt_params(ctx.get(), r.params.beta.empty() ? nullptr : r.params.beta.data(), &r.params.kappa_s,
+                             &r.params.gamma));
+    return r;
+}
+
+// inverse.hpp:80-88 / inverse.cpp:69-101 (the occupancy test runs on the device)
+struct CarveResult {
+    std::vector<uint8_t> mask;
+    ParamSet initial;
+};
+inline CarveResult space_carve(Context& ctx, const Scene& scene, const ImageSet& gt, double threshold_fraction,
+                               double fill_extinction) {
+    ctx.use(scene);
+    std::vector<double> g = detail::flatten(gt);
+    const size_t V = scene.species.empty() ? 0 : (size_t)scene.species[0].extinction.geom.voxel_count();
+    CarveResult r;
+    r.mask.assign(V, 0);
+    r.initial.beta.assign(V, 0.0);
+    check(prc_gpu_space_carve(ctx.get(), g.data(), threshold_fraction, fill_extinction, r.mask.data(),
+                              r.initial.beta.data()));
+    return r;
+}
+
+// inverse.hpp:97-106
+struct Metrics {
+    double eps = 0.0, delta = 0.0;
+};
+inline Metrics metrics(const std::vector<double>& estimate, const std::vector<double>& truth) {
+    if (estimate.size() != truth.size()) throw std::invalid_argument("metrics: dimension mismatch");
+    Metrics m;
+    check(prc_gpu_metrics(estimate.data(), truth.data(), truth.size(), &m.eps, &m.delta));
+    return m;
+}
+inline ImageSet downsample_images(const ImageSet& images, int rows, int cols) {
+    std::vector<int> r, c;
+    for (const auto& im : images) {
+        r.push_back(im.rows);
+        c.push_back(im.cols);
+    }
+    std::vector<double> in = detail::flatten(images), out(images.size() * (size_t)rows * cols);
+    check(prc_gpu_downsample_images((int)images.size(), r.data(), c.data(), in.data(), rows, cols, out.data()));
+    ImageSet o;
+    for (size_t k = 0; k < images.size(); ++k) {
+        Image im;
+        im.rows = rows;
+        im.cols = cols;
+        im.data.assign(out.begin() + (long)(k * rows * cols), out.begin() + (long)((k + 1) * rows * cols));
+        o.push_back(std::move(im));
+    }
+    return o;
 }
 
 }  // namespace pathrec_gpu

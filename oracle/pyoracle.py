@@ -204,6 +204,11 @@ class Reference:
         L.ref_reconstruct.argtypes = [C.c_void_p, C.c_void_p, _dp, C.c_double, _dp, C.c_int,
                                       C.c_uint64, C.c_uint64, C.c_int, C.c_int, C.c_int, _dp, _dp,
                                       _dp, _dp, _u64p]
+        L.ref_space_carve.argtypes = [C.c_void_p, _dp, C.c_double, C.c_double, C.POINTER(C.c_uint8), _dp]
+        L.ref_downsample.argtypes = [C.c_int, _i32p, _i32p, _dp, C.c_int, C.c_int, _dp]
+        L.ref_metrics.argtypes = [_dp, _dp, C.c_uint64, _dp, _dp]
+        L.ref_save_grid.argtypes = [C.c_char_p, _i32p, _dp, _dp, C.c_int, _dp]
+        L.ref_save_csv.argtypes = [C.c_char_p, C.c_int, _i32p, _dp, _dp, _dp, _dp, _i32p]
 
     def _err(self):
         return self.lib.ref_last_error().decode()
@@ -301,3 +306,49 @@ class Reference:
             raise ValueError(self._err())
         return dict(loss=loss, beta=beta[:scene.voxel_count], kappa_s=k.value, gamma=g.value,
                     sampling_phases=int(ph_.value))
+
+    # -------------------------------------------------- the driver around the loop (§8(f) 1)
+    def space_carve(self, scene: Scene, gt: np.ndarray, thr: float, fill: float):
+        h = scene.desc()
+        gt = np.ascontiguousarray(gt, dtype=np.float64)
+        V = scene.voxel_count
+        mask = np.zeros(max(V, 1), np.uint8)
+        beta = np.zeros(max(V, 1))
+        if self.lib.ref_space_carve(h.ptr, _ptr(gt, _dp), thr, fill, mask.ctypes.data_as(C.POINTER(C.c_uint8)),
+                                    _ptr(beta, _dp)):
+            raise ValueError(self._err())
+        return mask[:V], beta[:V]
+
+    def downsample(self, images, ro: int, co: int):
+        rows = np.array([im.shape[0] for im in images], np.int32)
+        cols = np.array([im.shape[1] for im in images], np.int32)
+        flat = np.ascontiguousarray(np.concatenate([np.asarray(im, np.float64).reshape(-1) for im in images]))
+        out = np.zeros(len(images) * ro * co)
+        if self.lib.ref_downsample(len(images), _ptr(rows, _i32p), _ptr(cols, _i32p), _ptr(flat, _dp), ro, co,
+                                   _ptr(out, _dp)):
+            raise ValueError(self._err())
+        return [out[k * ro * co:(k + 1) * ro * co].reshape(ro, co) for k in range(len(images))]
+
+    def metrics(self, e, t):
+        e = np.ascontiguousarray(e, dtype=np.float64)
+        t = np.ascontiguousarray(t, dtype=np.float64)
+        a, b = C.c_double(), C.c_double()
+        if self.lib.ref_metrics(_ptr(e, _dp), _ptr(t, _dp), t.size, C.byref(a), C.byref(b)):
+            raise ValueError(self._err())
+        return a.value, b.value
+
+    def save_grid(self, path: str, dims, origin, vs, values, unit: int = 0):
+        d = np.array(dims, np.int32)
+        o = np.array(origin, np.float64)
+        v = np.array(vs, np.float64)
+        x = np.ascontiguousarray(values, dtype=np.float64)
+        if self.lib.ref_save_grid(path.encode(), _ptr(d, _i32p), _ptr(o, _dp), _ptr(v, _dp), unit, _ptr(x, _dp)):
+            raise ValueError(self._err())
+
+    def save_csv(self, path: str, history):
+        n = len(history)
+        it = np.ascontiguousarray(history["iter"], np.int32)
+        st = np.ascontiguousarray(history["stage"], np.int32)
+        cols = [np.ascontiguousarray(history[k], np.float64) for k in ("time_s", "loss", "eps", "delta")]
+        if self.lib.ref_save_csv(path.encode(), n, _ptr(it, _i32p), *[_ptr(c, _dp) for c in cols], _ptr(st, _i32p)):
+            raise ValueError(self._err())

@@ -18,6 +18,7 @@
 
 #include "pathrec/gradient.hpp"
 #include "pathrec/inverse.hpp"
+#include "pathrec/io.hpp"
 #include "pathrec/pathstore.hpp"
 #include "pathrec/transport.hpp"
 #include "pathrec/traverse.hpp"
@@ -350,6 +351,82 @@ int ref_reconstruct(const prc_scene_desc* d, const prc_gpu_params* initial, cons
         if (kappa_out) *kappa_out = r.params.kappa_s;
         if (gamma_out) *gamma_out = r.params.gamma;
         if (phases_out) *phases_out = r.sampling_phases;
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+/* space_carve (inverse.cpp:69-101): mask (V bytes) and initial beta (V doubles). */
+int ref_space_carve(const prc_scene_desc* d, const double* gt, double thr, double fill, uint8_t* mask,
+                    double* beta) {
+    try {
+        Scene s = make_scene(d);
+        CarveResult r = space_carve(s, images_from(s, gt), thr, fill);
+        for (size_t v = 0; v < r.mask.size(); ++v) {
+            mask[v] = r.mask[v];
+            beta[v] = r.initial.beta[v];
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+/* downsample_images (inverse.cpp:116-133) over n images of rows[k] x cols[k]. */
+int ref_downsample(int n, const int* rows, const int* cols, const double* in, int ro, int co, double* out) {
+    try {
+        ImageSet im;
+        size_t k = 0;
+        for (int i = 0; i < n; ++i) {
+            Image x = Image::zeros(rows[i], cols[i]);
+            for (auto& px : x.data) px = in[k++];
+            im.push_back(std::move(x));
+        }
+        ImageSet r = downsample_images(im, ro, co);
+        size_t o = 0;
+        for (const auto& x : r)
+            for (double px : x.data) out[o++] = px;
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+/* metrics (inverse.cpp:103-114). */
+int ref_metrics(const double* e, const double* t, uint64_t n, double* eps, double* delta) {
+    try {
+        Metrics m = metrics(std::vector<double>(e, e + n), std::vector<double>(t, t + n));
+        *eps = m.eps;
+        *delta = m.delta;
+        return 0;
+    } catch (const std::exception& ex) {
+        return fail(ex);
+    }
+}
+
+/* save_grid (io.cpp:59-76) and save_csv (io.cpp:147-155) writers, for byte comparisons. */
+int ref_save_grid(const char* path, const int* dims, const double* origin, const double* vs, int unit,
+                  const double* values) {
+    try {
+        VoxelGridField f;
+        f.geom.dims = {dims[0], dims[1], dims[2]};
+        f.geom.origin = {origin[0], origin[1], origin[2]};
+        f.geom.voxel_size = {vs[0], vs[1], vs[2]};
+        f.values.assign(values, values + (size_t)dims[0] * dims[1] * dims[2]);
+        save_grid(f, static_cast<LengthUnit>(unit), path);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int ref_save_csv(const char* path, int n, const int* iter, const double* time_s, const double* loss,
+                 const double* eps, const double* delta, const int* stage) {
+    try {
+        std::vector<IterationLog> rows((size_t)n);
+        for (int i = 0; i < n; ++i) rows[(size_t)i] = {iter[i], time_s[i], loss[i], eps[i], delta[i], stage[i]};
+        save_csv(rows, path);
         return 0;
     } catch (const std::exception& e) {
         return fail(e);

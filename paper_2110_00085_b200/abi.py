@@ -90,3 +90,20 @@ class AdamConfig(C.Structure):
 class ReconstructOpts(C.Structure):
     _fields_ = [("seed", C.c_uint64), ("n_paths", C.c_uint64), ("max_bounces", C.c_int),
                 ("recycle_period", C.c_int), ("max_iterations", C.c_int)]
+
+
+class Stage(C.Structure):  # prc_gpu_stage (Stage, inverse.hpp:23-26)
+    _fields_ = [("rows", C.c_int), ("cols", C.c_int), ("n_paths", C.c_uint64)]
+
+
+class Schedule(C.Structure):  # prc_gpu_schedule (Schedule + ReconstructOptions, inverse.hpp:28-76)
+    _fields_ = [("seed", C.c_uint64), ("max_bounces", C.c_int), ("recycle_period", C.c_int),
+                ("max_iterations", C.c_int), ("stages", C.POINTER(Stage)), ("n_stages", C.c_int),
+                ("saturation_window", C.c_int), ("saturation_rel_improvement", C.c_double),
+                ("checkpoint_every", C.c_int), ("checkpoint_dir", C.c_char_p), ("length_unit", C.c_int),
+                ("truth", C.POINTER(Params))]
+
+
+class IterationLog(C.Structure):  # prc_gpu_iteration_log (IterationLog, inverse.hpp:46-53)
+    _fields_ = [("iter", C.c_int), ("time_s", C.c_double), ("loss", C.c_double), ("eps", C.c_double),
+                ("delta", C.c_double), ("stage", C.c_int)]

@@ -10,6 +10,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -118,6 +119,7 @@ struct prc_gpu_ctx {
     std::vector<double> host_sp;  // n_species x V (scene values)
     DBuf<double> scene_sp;        // device copy
     std::vector<prc_surface_desc> surfaces;
+    std::vector<prc_detector_desc> det_desc;  // as uploaded (stage schedules re-finalize)
     double scene_kappa = 0.0, scene_gamma = 0.0;
     // evaluation scratch
     DBuf<float> sp_t, bt_tot, dbeta;
@@ -265,6 +267,33 @@ int classify(const std::exception& e) {
 void begin(prc_gpu_ctx* c) { CK(cudaSetDevice(c->device)); }
 
 // ----------------------------------------------------------------------- scene upload
+// Detector::finalize (scene.cpp:8-14) for every detector, at the resolution of the
+// descriptor or rows[k] x cols[k] when given; assigns image offsets, returns n_pix.
+long long finalize_detectors(DScene& s, const prc_detector_desc* dd, int n, const int* rows, const int* cols) {
+    long long off = 0;
+    for (int k = 0; k < n; ++k) {
+        const prc_detector_desc& q = dd[k];
+        const int nr = rows ? rows[k] : q.rows, nc = cols ? cols[k] : q.cols;
+        if (nr <= 0 || nc <= 0) throw Err(PRC_ERR_CONFIG, "detector: non-positive pixel grid");
+        DDet& t = s.det[k];
+        const H3 dir = hnormalized(h3(q.direction));
+        const H3 right = hnormalized(hcross(dir, h3(q.up)));
+        const H3 up = hcross(right, dir);
+        put3(t.pos, h3(q.position));
+        put3(t.dir, dir);
+        put3(t.right, right);
+        put3(t.up, up);
+        t.hw = std::tan(0.5 * q.fov);
+        t.hh = t.hw * static_cast<double>(nr) / static_cast<double>(nc);
+        t.rows = nr;
+        t.cols = nc;
+        t.img_off = off;
+        off += (long long)nr * nc;
+    }
+    s.n_pix = off;
+    return off;
+}
+
 void upload_scene(prc_gpu_ctx* c, const prc_scene_desc* d) {
     if (d->n_species < 0 || d->n_species > PRC_MAX_SPECIES)
         throw Err(PRC_ERR_CONFIG, "scene: species count outside 0..16");
@@ -354,25 +383,7 @@ void upload_scene(prc_gpu_ctx* c, const prc_scene_desc* d) {
     s.prefactor = s.light_kind == 1 ? PRC_FOUR_PI * s.radiance
                                     : (s.bmax[0] - s.bmin[0]) * (s.bmax[1] - s.bmin[1]) * s.radiance;
     s.n_det = d->n_detectors;
-    long long off = 0;
-    for (int k = 0; k < d->n_detectors; ++k) {  // Detector::finalize, scene.cpp:8-14
-        const prc_detector_desc& q = d->detectors[k];
-        if (q.rows <= 0 || q.cols <= 0) throw Err(PRC_ERR_CONFIG, "detector: non-positive pixel grid");
-        DDet& t = s.det[k];
-        const H3 dir = hnormalized(h3(q.direction));
-        const H3 right = hnormalized(hcross(dir, h3(q.up)));
-        const H3 up = hcross(right, dir);
-        put3(t.pos, h3(q.position));
-        put3(t.dir, dir);
-        put3(t.right, right);
-        put3(t.up, up);
-        t.hw = std::tan(0.5 * q.fov);
-        t.hh = t.hw * static_cast<double>(q.rows) / static_cast<double>(q.cols);
-        t.rows = q.rows;
-        t.cols = q.cols;
-        t.img_off = off;
-        off += (long long)q.rows * q.cols;
-    }
+    const long long off = finalize_detectors(s, d->detectors, d->n_detectors, nullptr, nullptr);
     s.n_pix = off;
     // Guard-free walks over the padded layout (prc_device.cuh, dda_walk_pad): exact when
     // the rounding of the tmax sums (~512 ulp of a distance <= 4R) stays far below a voxel.
@@ -399,6 +410,7 @@ void upload_scene(prc_gpu_ctx* c, const prc_scene_desc* d) {
     c->n_pix = off;
     c->host_sp.swap(sp);
     c->surfaces.assign(d->surfaces, d->surfaces + d->n_surfaces);
+    c->det_desc.assign(d->detectors, d->detectors + d->n_detectors);
     c->scene_sp.alloc(c->host_sp.size());
     if (!c->host_sp.empty())
         CK(cudaMemcpy(c->scene_sp.p, c->host_sp.data(), c->host_sp.size() * sizeof(double),
@@ -1363,6 +1375,18 @@ PRC_EXPORT int prc_gpu_scene_pixel_count(const prc_gpu_ctx* ctx, uint64_t* out) 
     return PRC_OK;
 }
 
+// Sum of a per-rank counter over the communicator (exact below 2^53).
+static uint64_t global_count(prc_gpu_ctx* ctx, uint64_t local) {
+    double t = (double)local;
+    if (ctx->comm) {
+        CK(cudaMemcpy(ctx->loss.p, &t, 8, cudaMemcpyHostToDevice));
+        ctx->allreduce(ctx->loss.p, 1);
+        ctx->sync();
+        CK(cudaMemcpy(&t, ctx->loss.p, 8, cudaMemcpyDeviceToHost));
+    }
+    return (uint64_t)t;
+}
+
 PRC_EXPORT int prc_gpu_render(prc_gpu_ctx* ctx, const prc_gpu_render_opts* opts,
                               const prc_gpu_params* params, double* images_out,
                               uint64_t* truncated_out, prc_gpu_store** store_out) {
@@ -1393,16 +1417,7 @@ PRC_EXPORT int prc_gpu_render(prc_gpu_ctx* ctx, const prc_gpu_render_opts* opts,
     CK(launch_scale(ctx->images.p, ctx->n_pix, 1.0 / (double)opts->n_paths, ctx->stream, &ctx->launches));
     copy_out(ctx, images_out, ctx->images.p, (size_t)ctx->n_pix);
     ctx->sync();
-    if (truncated_out) {
-        double t = (double)st->truncated;
-        if (ctx->comm) {
-            CK(cudaMemcpy(ctx->loss.p, &t, 8, cudaMemcpyHostToDevice));
-            ctx->allreduce(ctx->loss.p, 1);
-            ctx->sync();
-            CK(cudaMemcpy(&t, ctx->loss.p, 8, cudaMemcpyDeviceToHost));
-        }
-        *truncated_out = (uint64_t)t;
-    }
+    if (truncated_out) *truncated_out = global_count(ctx, st->truncated);
     if (store_out) *store_out = st.release();
     ABI_CATCH
 }
@@ -1729,6 +1744,318 @@ PRC_EXPORT int prc_gpu_reconstruct(prc_gpu_ctx* ctx, const prc_gpu_params* initi
     }
     if (phases_out) *phases_out = phases;
     ABI_CATCH
+}
+
+// ----------------------------------------------------------- Algorithm-2 driver (§8(f) 1)
+// Host utilities in the reference's arithmetic order (inverse.cpp:103-133, io.cpp:32-76,
+// 147-155); the carve test runs on the device.
+
+static void downsample(int n_img, const int* rows, const int* cols, const double* in, int ro, int co,
+                       double* out) {  // downsample_images, inverse.cpp:116-133
+    size_t ii = 0, oo = 0;
+    for (int k = 0; k < n_img; ++k) {
+        const int r0 = rows[k], c0 = cols[k];
+        double* o = out + oo;
+        if (r0 == ro && c0 == co) {
+            std::memcpy(o, in + ii, (size_t)r0 * c0 * 8);
+        } else {
+            std::fill(o, o + (size_t)ro * co, 0.0);
+            for (int r = 0; r < r0; ++r) {
+                const int cr = r * ro / r0;
+                for (int c = 0; c < c0; ++c) o[(size_t)cr * co + (size_t)(c * co / c0)] += in[ii + (size_t)r * c0 + c];
+            }
+        }
+        ii += (size_t)r0 * c0;
+        oo += (size_t)ro * co;
+    }
+}
+
+static void metrics_host(const double* e, const double* t, uint64_t n, double* eps, double* delta) {
+    double diff = 0.0, nt = 0.0, ne = 0.0;  // inverse.cpp:103-114
+    for (uint64_t i = 0; i < n; ++i) {
+        diff += std::abs(t[i] - e[i]);
+        nt += std::abs(t[i]);
+        ne += std::abs(e[i]);
+    }
+    if (nt == 0.0) throw Err(PRC_ERR_CONFIG, "metrics: zero-norm truth");
+    *eps = diff / nt;
+    *delta = (nt - ne) / nt;
+}
+
+template <class T>
+static void put_raw(std::ofstream& os, const T& v) {
+    os.write(reinterpret_cast<const char*>(&v), sizeof(T));
+}
+
+static void save_grid_host(const std::string& path, const int dims[3], const double org[3], const double vs[3],
+                           int unit, const double* values) {  // save_grid, io.cpp:59-76
+    std::ofstream os(path, std::ios::binary);
+    if (!os) throw Err(PRC_ERR_IO, "save_grid: cannot open " + path);
+    os.write("VGRD", 4);
+    put_raw<uint32_t>(os, 1u);
+    for (int a = 0; a < 3; ++a) put_raw<uint32_t>(os, (uint32_t)dims[a]);
+    for (int a = 0; a < 3; ++a) put_raw<double>(os, org[a]);
+    for (int a = 0; a < 3; ++a) put_raw<double>(os, vs[a]);
+    put_raw<uint8_t>(os, (uint8_t)unit);
+    const size_t n = (size_t)dims[0] * dims[1] * dims[2];
+    for (size_t i = 0; i < n; ++i) put_raw<float>(os, (float)values[i]);
+    if (!os) throw Err(PRC_ERR_IO, "save_grid: write failure on " + path);
+}
+
+static void save_csv_host(const std::vector<prc_gpu_iteration_log>& rows, const std::string& path) {
+    std::ofstream os(path);  // save_csv, io.cpp:147-155
+    if (!os) throw Err(PRC_ERR_IO, "save_csv: cannot open " + path);
+    os << "iter,time_s,loss,eps,delta,stage\r\n";
+    os.precision(17);
+    for (const auto& r : rows)
+        os << r.iter << "," << r.time_s << "," << r.loss << "," << r.eps << "," << r.delta << "," << r.stage << "\r\n";
+}
+
+// Re-finalizes every detector at rows[k] x cols[k] and resizes the pixel buffers.
+static void set_resolution(prc_gpu_ctx* c, const std::vector<int>& rows, const std::vector<int>& cols) {
+    const long long n_pix = finalize_detectors(c->dsc, c->det_desc.data(), (int)c->det_desc.size(), rows.data(),
+                                               cols.data());
+    c->n_pix = n_pix;
+    c->images.alloc((size_t)n_pix);
+    c->weights.alloc((size_t)n_pix);
+    c->opt_gt.alloc((size_t)n_pix);
+    ++c->fwd_gen;
+}
+
+PRC_EXPORT int prc_gpu_reconstruct_schedule(prc_gpu_ctx* ctx, const prc_gpu_params* initial,
+                                            const double* gt_images, const prc_gpu_adam_config* adam,
+                                            const prc_gpu_schedule* sch, prc_gpu_iteration_log* history,
+                                            uint64_t* phases_out, uint64_t* truncated_out) {
+    if (!ctx || !gt_images || !sch) return fail(PRC_ERR_INVALID, "prc_gpu_reconstruct_schedule: null argument");
+    if (sch->n_stages < 1 || !sch->stages)
+        return fail(PRC_ERR_CONFIG, "reconstruct: schedule needs at least one stage");
+    ABI_TRY
+    begin(ctx);
+    ctx->check_scene();
+    const auto t_start = std::chrono::steady_clock::now();
+    const int n_det = ctx->dsc.n_det;
+    std::vector<int> base_rows(n_det), base_cols(n_det);
+    for (int k = 0; k < n_det; ++k) {
+        base_rows[k] = ctx->dsc.det[k].rows;
+        base_cols[k] = ctx->dsc.det[k].cols;
+    }
+    const std::vector<double> gt_full(gt_images, gt_images + ctx->n_pix);
+    struct Restore {  // the scene's own resolution and ground truth come back on every exit
+        prc_gpu_ctx* c;
+        const std::vector<int>& r;
+        const std::vector<int>& k;
+        const std::vector<double>& gt;
+        ~Restore() {
+            try {
+                set_resolution(c, r, k);
+                CK(cudaMemcpyAsync(c->opt_gt.p, gt.data(), gt.size() * 8, cudaMemcpyHostToDevice, c->stream));
+                c->sync();
+            } catch (...) {
+                c->opt_ready = false;
+            }
+        }
+    } restore{ctx, base_rows, base_cols, gt_full};
+    opt_init(ctx, initial, gt_full.data(), adam);
+    std::vector<double> truth;
+    if (sch->truth) {
+        if (ctx->opt_mode == 0) {
+            if (!sch->truth->beta || (long long)sch->truth->n_beta != ctx->V)
+                throw Err(PRC_ERR_CONFIG, "truth beta size != voxel count");
+            truth.assign(sch->truth->beta, sch->truth->beta + ctx->V);
+        } else {
+            truth = {sch->truth->kappa_s, sch->truth->gamma};
+        }
+    }
+    const bool ckpt = sch->checkpoint_dir && sch->checkpoint_dir[0] && sch->checkpoint_every > 0;
+    const bool want_x = !truth.empty() || ckpt;
+    std::vector<double> x_host;
+    std::vector<prc_gpu_iteration_log> rows;
+    std::vector<double> loss_hist;
+    const int n_r = std::max(1, sch->recycle_period);
+    const int w = sch->saturation_window > 0 ? sch->saturation_window : 20;
+    const double rel = sch->saturation_rel_improvement;
+    int stage = 0, applied = -1, pending = 0, stage_start = 0;
+    uint64_t phases = 0, truncated = 0;
+    std::vector<int> cur_rows = base_rows, cur_cols = base_cols;
+    std::unique_ptr<prc_gpu_store> store;
+    for (int t = 0; t < sch->max_iterations; ++t) {
+        if (t % n_r == 0) {  // resample boundary (inverse.cpp:175-205)
+            if (pending != applied) {
+                stage = pending;
+                applied = stage;
+                stage_start = t;
+                const prc_gpu_stage& st = sch->stages[stage];
+                for (int k = 0; k < n_det; ++k) {
+                    if (st.rows > 0) cur_rows[k] = st.rows;
+                    if (st.cols > 0) cur_cols[k] = st.cols;
+                }
+                store.reset();
+                set_resolution(ctx, cur_rows, cur_cols);
+                std::vector<double> g((size_t)ctx->n_pix);
+                downsample(n_det, base_rows.data(), base_cols.data(), gt_full.data(), cur_rows[0], cur_cols[0],
+                           g.data());
+                if ((long long)g.size() != ctx->n_pix)
+                    throw Err(PRC_ERR_CONFIG, "reconstruct: stage resolution must be the same for every detector");
+                CK(cudaMemcpyAsync(ctx->opt_gt.p, g.data(), g.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+            }
+            store.reset();
+            bind_trace_species(ctx);
+            double kg[2] = {ctx->scene_kappa, ctx->scene_gamma};
+            if (ctx->opt_mode == 1) {
+                CK(cudaMemcpyAsync(kg, ctx->opt_x.p, 16, cudaMemcpyDeviceToHost, ctx->stream));
+                ctx->sync();
+            }
+            const uint64_t n_paths = sch->stages[stage].n_paths;
+            if (n_paths == 0) throw Err(PRC_ERR_CONFIG, "reconstruct: stage n_paths must be >= 1");
+            prc_gpu_render_opts ro{n_paths, sch->seed + 0x9E3779B97F4A7C15ull * (phases + 1),
+                                   sch->max_bounces > 0 ? sch->max_bounces : 500, -1};
+            store = trace_store(ctx, &ro, ctx->trace_sp.p, kg[0], kg[1], nullptr, true);
+            truncated += global_count(ctx, store->truncated);
+            sort_store(ctx, store.get());
+            store->generation = (uint64_t)t;
+            ++phases;
+        }
+        if (want_x) {  // the unknowns before this iteration's update (inverse.cpp:215-236)
+            x_host.resize((size_t)ctx->opt_n);
+            CK(cudaMemcpyAsync(x_host.data(), ctx->opt_x.p, x_host.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+            ctx->sync();
+        }
+        const double l = opt_step(ctx, store.get());  // loss, gradient, ADAM
+        loss_hist.push_back(l);
+        prc_gpu_iteration_log row{};
+        row.iter = t;
+        row.time_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+        row.loss = l;
+        row.stage = stage;
+        if (!truth.empty()) metrics_host(x_host.data(), truth.data(), truth.size(), &row.eps, &row.delta);
+        rows.push_back(row);
+        if (history) history[t] = row;
+        if (ckpt && (t + 1) % sch->checkpoint_every == 0) {
+            const std::string dir(sch->checkpoint_dir);
+            if (ctx->opt_mode == 0 && ctx->dsc.has_medium)
+                save_grid_host(dir + "/checkpoint_" + std::to_string(t) + ".vgrd", ctx->dsc.dims, ctx->dsc.gorg,
+                               ctx->dsc.vs, sch->length_unit, x_host.data());
+            save_csv_host(rows, dir + "/loss.csv");
+        }
+        // stage saturation (inverse.cpp:249-258)
+        const int since = t - stage_start;
+        if (pending == stage && stage + 1 < sch->n_stages && since >= w) {
+            const double past = loss_hist[(size_t)(t - w)], now = loss_hist.back();
+            if (past > 0.0 && (past - now) / past < rel) pending = stage + 1;
+        }
+    }
+    if (phases_out) *phases_out = phases;
+    if (truncated_out) *truncated_out = truncated;
+    ABI_CATCH
+}
+
+PRC_EXPORT int prc_gpu_space_carve(prc_gpu_ctx* ctx, const double* gt_images, double threshold_fraction,
+                                   double fill_extinction, uint8_t* mask_out, double* beta_out) {
+    if (!ctx || !gt_images) return fail(PRC_ERR_INVALID, "prc_gpu_space_carve: null argument");
+    ABI_TRY
+    begin(ctx);
+    ctx->check_scene();
+    const DScene& s = ctx->dsc;
+    if (s.n_det < 2) throw Err(PRC_ERR_INVALID, "space_carve: needs at least 2 detectors");
+    if (!s.has_medium) throw Err(PRC_ERR_INVALID, "space_carve: scene has no medium");
+    std::vector<double> thr((size_t)s.n_det, 0.0);
+    for (int k = 0; k < s.n_det; ++k) {  // view maxima (inverse.cpp:76-78)
+        double mx = 0.0;
+        const long long n = (long long)s.det[k].rows * s.det[k].cols;
+        for (long long p = 0; p < n; ++p) mx = std::max(mx, gt_images[s.det[k].img_off + p]);
+        thr[(size_t)k] = threshold_fraction * mx;
+    }
+    cudaStream_t q = ctx->stream;
+    DBuf<double> dgt, dthr, dbeta;
+    DBuf<uint8_t> dmask;
+    dgt.alloc((size_t)ctx->n_pix);
+    dthr.alloc(thr.size());
+    dmask.alloc((size_t)ctx->V);
+    dbeta.alloc((size_t)ctx->V);
+    CK(cudaMemcpyAsync(dgt.p, gt_images, (size_t)ctx->n_pix * 8, cudaMemcpyHostToDevice, q));
+    CK(cudaMemcpyAsync(dthr.p, thr.data(), thr.size() * 8, cudaMemcpyHostToDevice, q));
+    CK(launch_space_carve(s, dgt.p, dthr.p, fill_extinction, dmask.p, dbeta.p, q, &ctx->launches));
+    if (mask_out) CK(cudaMemcpyAsync(mask_out, dmask.p, (size_t)ctx->V, cudaMemcpyDeviceToHost, q));
+    if (beta_out) CK(cudaMemcpyAsync(beta_out, dbeta.p, (size_t)ctx->V * 8, cudaMemcpyDeviceToHost, q));
+    ctx->sync();
+    ABI_CATCH
+}
+
+PRC_EXPORT int prc_gpu_metrics(const double* estimate, const double* truth, uint64_t n, double* eps,
+                               double* delta) {
+    if (!estimate || !truth || !eps || !delta) return fail(PRC_ERR_INVALID, "prc_gpu_metrics: null argument");
+    try {
+        metrics_host(estimate, truth, n, eps, delta);
+        return PRC_OK;
+    } catch (const Err& e) {
+        return fail(e.code, e.what());
+    }
+}
+
+PRC_EXPORT int prc_gpu_downsample_images(int n_images, const int* rows, const int* cols, const double* images,
+                                         int rows_out, int cols_out, double* out) {
+    if (!rows || !cols || !images || !out) return fail(PRC_ERR_INVALID, "prc_gpu_downsample_images: null argument");
+    if (n_images < 0 || rows_out <= 0 || cols_out <= 0) return fail(PRC_ERR_CONFIG, "downsample: bad sizes");
+    for (int k = 0; k < n_images; ++k)
+        if (rows[k] <= 0 || cols[k] <= 0) return fail(PRC_ERR_CONFIG, "downsample: bad image size");
+    downsample(n_images, rows, cols, images, rows_out, cols_out, out);
+    return PRC_OK;
+}
+
+PRC_EXPORT int prc_gpu_save_grid(const char* path, const int dims[3], const prc_vec3* origin,
+                                 const prc_vec3* voxel_size, int length_unit, const double* values) {
+    if (!path || !dims || !origin || !voxel_size || !values) return fail(PRC_ERR_INVALID, "prc_gpu_save_grid: null argument");
+    try {
+        const double o[3] = {origin->x, origin->y, origin->z}, v[3] = {voxel_size->x, voxel_size->y, voxel_size->z};
+        save_grid_host(path, dims, o, v, length_unit, values);
+        return PRC_OK;
+    } catch (const Err& e) {
+        return fail(e.code, e.what());
+    }
+}
+
+template <class T>
+static T get_raw(std::ifstream& is) {
+    T v{};
+    is.read(reinterpret_cast<char*>(&v), sizeof(T));
+    return v;
+}
+
+PRC_EXPORT int prc_gpu_load_grid(const char* path, int dims_out[3], prc_vec3* origin_out, prc_vec3* voxel_size_out,
+                                 int* length_unit_out, double* values_out, uint64_t capacity) {
+    if (!path) return fail(PRC_ERR_INVALID, "prc_gpu_load_grid: null path");
+    std::ifstream is(path, std::ios::binary);  // load_grid, io.cpp:32-57
+    if (!is) return fail(PRC_ERR_IO, std::string("load_grid: cannot open ") + path);
+    char magic[4];
+    is.read(magic, 4);
+    if (!is || std::memcmp(magic, "VGRD", 4) != 0)
+        return fail(PRC_ERR_IO, std::string("load_grid: bad magic at offset 0 in ") + path);
+    if (get_raw<uint32_t>(is) != 1u) return fail(PRC_ERR_IO, std::string("load_grid: unsupported version in ") + path);
+    int dims[3];
+    for (int a = 0; a < 3; ++a) {
+        const uint32_t d = get_raw<uint32_t>(is);
+        if (d == 0 || d > (1u << 20)) return fail(PRC_ERR_IO, std::string("load_grid: bad dims in ") + path);
+        dims[a] = (int)d;
+    }
+    double o[3], v[3];
+    for (int a = 0; a < 3; ++a) o[a] = get_raw<double>(is);
+    for (int a = 0; a < 3; ++a) v[a] = get_raw<double>(is);
+    const uint8_t tag = get_raw<uint8_t>(is);
+    if (tag > 1) return fail(PRC_ERR_IO, std::string("load_grid: bad unit tag in ") + path);
+    const uint64_t count = (uint64_t)dims[0] * dims[1] * dims[2];
+    std::vector<float> raw(count);
+    is.read(reinterpret_cast<char*>(raw.data()), (std::streamsize)(count * sizeof(float)));
+    if (!is) return fail(PRC_ERR_IO, std::string("load_grid: truncated payload in ") + path);
+    if (dims_out)
+        for (int a = 0; a < 3; ++a) dims_out[a] = dims[a];
+    if (origin_out) *origin_out = prc_vec3{o[0], o[1], o[2]};
+    if (voxel_size_out) *voxel_size_out = prc_vec3{v[0], v[1], v[2]};
+    if (length_unit_out) *length_unit_out = tag;
+    if (values_out) {
+        if (capacity < count) return fail(PRC_ERR_INVALID, "load_grid: capacity too small");
+        for (uint64_t i = 0; i < count; ++i) values_out[i] = raw[i];
+    }
+    return PRC_OK;
 }
 
 PRC_EXPORT int prc_gpu_last_timings(const prc_gpu_ctx* ctx, double* ms8) {

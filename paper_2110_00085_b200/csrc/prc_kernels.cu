@@ -627,6 +627,25 @@ __global__ void k_walk(const __grid_constant__ DScene sc, const double* rays, lo
     if (!off) counts[i] = c;
 }
 
+// space_carve (inverse.cpp:69-101): voxel centre (grid.hpp:56-62, same operation order)
+// projected into every detector; occupied when every view sees it above the threshold.
+__global__ void k_space_carve(const __grid_constant__ DScene sc, const double* __restrict__ gt,
+                              const double* __restrict__ thr, double fill, uint8_t* mask, double* beta) {
+    const long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= sc.V) return;
+    const int nx = sc.dims[0], ny = sc.dims[1];
+    const int ix = (int)(v % nx), iy = (int)((v / nx) % ny), iz = (int)(v / ((long long)nx * ny));
+    const V3 c = mk(sc.gorg[0] + ((double)ix + 0.5) * sc.vs[0], sc.gorg[1] + ((double)iy + 0.5) * sc.vs[1],
+                    sc.gorg[2] + ((double)iz + 0.5) * sc.vs[2]);
+    bool occupied = true;
+    for (int k = 0; k < sc.n_det && occupied; ++k) {
+        const int pixel = pixel_of(sc.det[k], c);
+        occupied = pixel >= 0 && gt[sc.det[k].img_off + pixel] > thr[k];
+    }
+    if (mask) mask[v] = occupied ? 1 : 0;
+    if (beta) beta[v] = occupied ? fill : 0.0;
+}
+
 __global__ void k_pixel_of(const __grid_constant__ DScene sc, int det, const double* pts, long long n,
                            int32_t* out) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -921,6 +940,13 @@ cudaError_t launch_walk(const DScene& sc, const double* rays, long long n, uint3
         k_walk<true><<<grid_for(n), kTPB, 0, s>>>(sc, rays, n, counts, off, vox, len);
     else
         k_walk<false><<<grid_for(n), kTPB, 0, s>>>(sc, rays, n, counts, off, vox, len);
+    LAUNCH_DONE();
+}
+
+cudaError_t launch_space_carve(const DScene& sc, const double* gt, const double* thr, double fill, uint8_t* mask,
+                               double* beta, cudaStream_t s, unsigned long long* launches) {
+    if (sc.V == 0) return cudaSuccess;
+    k_space_carve<<<grid_for(sc.V), kTPB, 0, s>>>(sc, gt, thr, fill, mask, beta);
     LAUNCH_DONE();
 }
 

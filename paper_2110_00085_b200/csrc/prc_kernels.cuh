@@ -187,6 +187,9 @@ cudaError_t launch_philox(unsigned long long seed, unsigned long long stream,
 cudaError_t launch_walk(const DScene& sc, const double* rays, long long n, uint32_t* counts,
                         const unsigned long long* offsets, uint32_t* vox, double* len,
                         cudaStream_t s, unsigned long long* launches, bool pad = false);
+// thr[k] = threshold_fraction * max of view k (host-computed, as inverse.cpp:76-80)
+cudaError_t launch_space_carve(const DScene& sc, const double* gt, const double* thr, double fill, uint8_t* mask,
+                               double* beta, cudaStream_t s, unsigned long long* launches);
 cudaError_t launch_pixel_of(const DScene& sc, int det, const double* pts, long long n,
                             int32_t* out, cudaStream_t s, unsigned long long* launches);
 // Per (interaction vertex, detector) event materialisation: valid, pixel, cos_le,

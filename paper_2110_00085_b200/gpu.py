@@ -106,6 +106,14 @@ def load_library(path: Optional[str] = None):
         "prc_gpu_opt_images": [vp, _dp],
         "prc_gpu_reconstruct": [vp, vp, _dp, C.POINTER(abi.AdamConfig),
                                 C.POINTER(abi.ReconstructOpts), _dp, _u64p],
+        "prc_gpu_reconstruct_schedule": [vp, vp, _dp, C.POINTER(abi.AdamConfig), C.POINTER(abi.Schedule),
+                                         C.POINTER(abi.IterationLog), _u64p, _u64p],
+        "prc_gpu_space_carve": [vp, _dp, C.c_double, C.c_double, C.POINTER(C.c_uint8), _dp],
+        "prc_gpu_metrics": [_dp, _dp, C.c_uint64, _dp, _dp],
+        "prc_gpu_downsample_images": [C.c_int, _i32p, _i32p, _dp, C.c_int, C.c_int, _dp],
+        "prc_gpu_save_grid": [C.c_char_p, _i32p, C.POINTER(abi.Vec3), C.POINTER(abi.Vec3), C.c_int, _dp],
+        "prc_gpu_load_grid": [C.c_char_p, _i32p, C.POINTER(abi.Vec3), C.POINTER(abi.Vec3),
+                              C.POINTER(C.c_int), _dp, C.c_uint64],
         "prc_gpu_last_timings": [vp, _dp],
         "prc_gpu_kernel_launches": [vp, _u64p],
         "prc_gpu_timer_start": [vp],
@@ -391,6 +399,47 @@ class Context:
                                         C.byref(ro), _ptr(loss, _dp), C.byref(phases)))
         return {"loss": loss, "params": self.opt_params(), "sampling_phases": int(phases.value)}
 
+    def reconstruct_schedule(self, scene: Optional[Scene], gt: np.ndarray, initial: Optional[ParamSet],
+                             stages, seed: int = 0, recycle_period: int = 30, max_iterations: int = 100,
+                             max_bounces: int = 500, alpha: float = 1e7, step_scale=None,
+                             saturation_window: int = 20, saturation_rel_improvement: float = 0.01,
+                             checkpoint_every: int = 0, checkpoint_dir: Optional[str] = None,
+                             length_unit: int = 0, truth: Optional[ParamSet] = None) -> dict:
+        """reconstruct() with a stage schedule (inverse.cpp:154-263).  stages: sequence of
+        (rows, cols, n_paths).  Returns the per-iteration history (iter, time_s, loss, eps,
+        delta, stage), the final unknowns and the sampling-phase / truncation counters."""
+        self._use(scene)
+        adam = _adam(alpha, 0.9, 0.999, 1e-8, True, step_scale)
+        gt = np.ascontiguousarray(gt, dtype=np.float64).reshape(-1)
+        ph = ParamsHolder(initial)
+        th = ParamsHolder(truth)
+        st = (abi.Stage * len(stages))(*[abi.Stage(int(r), int(c), int(n)) for r, c, n in stages])
+        sch = abi.Schedule(seed, max_bounces, recycle_period, max_iterations, st, len(stages),
+                           saturation_window, saturation_rel_improvement, checkpoint_every,
+                           checkpoint_dir.encode() if checkpoint_dir else None, length_unit,
+                           C.pointer(th.p) if truth is not None else None)
+        hist = (abi.IterationLog * max(1, max_iterations))()
+        phases, trunc = C.c_uint64(), C.c_uint64()
+        _check(_lib.prc_gpu_reconstruct_schedule(self.ptr, ph.ptr, _ptr(gt, _dp), C.byref(adam[0]), C.byref(sch),
+                                                 hist, C.byref(phases), C.byref(trunc)))
+        rows = [(h.iter, h.time_s, h.loss, h.eps, h.delta, h.stage) for h in hist[:max_iterations]]
+        return {"history": np.array(rows, dtype=[("iter", "i4"), ("time_s", "f8"), ("loss", "f8"), ("eps", "f8"),
+                                                 ("delta", "f8"), ("stage", "i4")]),
+                "params": self.opt_params(), "sampling_phases": int(phases.value),
+                "truncated_paths": int(trunc.value)}
+
+    def space_carve(self, scene: Optional[Scene], gt: np.ndarray, threshold_fraction: float,
+                    fill_extinction: float):
+        """space_carve (inverse.cpp:69-101) on the device: (mask, initial beta)."""
+        self._use(scene)
+        gt = np.ascontiguousarray(gt, dtype=np.float64).reshape(-1)
+        V = self.scene.voxel_count
+        mask = np.zeros(max(V, 1), np.uint8)
+        beta = np.zeros(max(V, 1))
+        _check(_lib.prc_gpu_space_carve(self.ptr, _ptr(gt, _dp), threshold_fraction, fill_extinction,
+                                        mask.ctypes.data_as(C.POINTER(C.c_uint8)), _ptr(beta, _dp)))
+        return mask[:V], beta[:V]
+
     # ------------------------------------------------------------------ diagnostics
     def last_timings(self) -> dict:
         ms = np.zeros(8)
@@ -441,6 +490,53 @@ class Context:
         _check(_lib.prc_gpu_debug_pixel_of(self.ptr, det, pts.shape[0], _ptr(pts, _dp),
                                            _ptr(out, _i32p)))
         return out
+
+
+def metrics(estimate: np.ndarray, truth: np.ndarray):
+    """metrics (inverse.cpp:103-114): (eps, delta)."""
+    load_library()
+    e = np.ascontiguousarray(estimate, dtype=np.float64)
+    t = np.ascontiguousarray(truth, dtype=np.float64)
+    if e.size != t.size:
+        raise PrcConfigError(abi.PRC_ERR_CONFIG, "metrics: dimension mismatch")
+    eps, delta = C.c_double(), C.c_double()
+    _check(_lib.prc_gpu_metrics(_ptr(e, _dp), _ptr(t, _dp), t.size, C.byref(eps), C.byref(delta)))
+    return eps.value, delta.value
+
+
+def downsample_images(images, rows_out: int, cols_out: int):
+    """downsample_images (inverse.cpp:116-133): list of 2-D arrays -> list of block sums."""
+    load_library()
+    rows = np.array([im.shape[0] for im in images], np.int32)
+    cols = np.array([im.shape[1] for im in images], np.int32)
+    flat = np.ascontiguousarray(np.concatenate([np.asarray(im, np.float64).reshape(-1) for im in images]))
+    out = np.zeros(len(images) * rows_out * cols_out)
+    _check(_lib.prc_gpu_downsample_images(len(images), _ptr(rows, _i32p), _ptr(cols, _i32p), _ptr(flat, _dp),
+                                          rows_out, cols_out, _ptr(out, _dp)))
+    return [out[k * rows_out * cols_out:(k + 1) * rows_out * cols_out].reshape(rows_out, cols_out)
+            for k in range(len(images))]
+
+
+def save_grid(path: str, dims, origin, voxel_size, values, length_unit: int = 0):
+    """VGRD v1 writer (io.cpp:59-76)."""
+    load_library()
+    d = np.array(dims, np.int32)
+    v = np.ascontiguousarray(values, dtype=np.float64)
+    _check(_lib.prc_gpu_save_grid(path.encode(), _ptr(d, _i32p), C.byref(abi.Vec3(*origin)),
+                                  C.byref(abi.Vec3(*voxel_size)), length_unit, _ptr(v, _dp)))
+
+
+def load_grid(path: str) -> dict:
+    """VGRD v1 reader (io.cpp:32-57)."""
+    load_library()
+    d = np.zeros(3, np.int32)
+    o, vs, unit = abi.Vec3(), abi.Vec3(), C.c_int()
+    _check(_lib.prc_gpu_load_grid(path.encode(), _ptr(d, _i32p), C.byref(o), C.byref(vs), C.byref(unit), None, 0))
+    vals = np.zeros(int(np.prod(d)))
+    _check(_lib.prc_gpu_load_grid(path.encode(), _ptr(d, _i32p), C.byref(o), C.byref(vs), C.byref(unit),
+                                  _ptr(vals, _dp), vals.size))
+    return {"dims": tuple(int(x) for x in d), "origin": (o.x, o.y, o.z), "voxel_size": (vs.x, vs.y, vs.z),
+            "unit": unit.value, "values": vals}
 
 
 def _adam(alpha, eta1, eta2, eps, nonneg, step_scale):

@@ -117,6 +117,28 @@ int main() {
     for (double l : res.loss) finite = finite && std::isfinite(l);
     for (double b : res.params.beta) moved = moved || b != 3.0;
     if (res.sampling_phases != 3 || !finite || !moved) return 8;
+    // the stage-scheduled loop: a coarse 4x4 stage, then the uploaded resolution
+    ScheduleOptions so;
+    so.adam.alpha = 0.05;
+    so.schedule.recycle_period = 4;
+    so.schedule.max_iterations = 12;
+    so.schedule.saturation_window = 3;
+    so.schedule.saturation_rel_improvement = 1.0;  // saturate as soon as the window is full
+    so.schedule.stages = {Stage{4, 4, 5000}, Stage{0, 0, 5000}};
+    ScheduleResult sr = reconstruct(ctx, s, gt, init, so);
+    std::printf("schedule: phases %llu stages %d..%d\n", (unsigned long long)sr.sampling_phases,
+                sr.history.front().stage, sr.history.back().stage);
+    if (sr.sampling_phases != 3 || sr.history.size() != 12 || sr.history[3].stage != 0 || sr.history[4].stage != 1)
+        return 9;
+    // metrics / downsample / carve
+    Metrics m = metrics({1.0, 2.0}, {1.0, 4.0});
+    if (std::fabs(m.eps - 0.4) > 1e-15 || std::fabs(m.delta - 0.4) > 1e-15) return 10;
+    ImageSet small = downsample_images(gt, 2, 2);
+    if (small.size() != gt.size() || small[0].data.size() != 4) return 11;
+    if (s.detectors.size() >= 2) {
+        CarveResult cr = space_carve(ctx, s, gt, 0.0, 1.5);
+        if (cr.mask.size() != 64) return 12;
+    }
     std::remove("host_api_test.pstr");
     return 0;
 }
