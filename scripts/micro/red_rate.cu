@@ -18,6 +18,7 @@ __global__ void k_red(T* g, uint32_t n_mask, int iters, int group, int mode) {
         uint32_t base = hash32(tid / (mode ? group : 1) * 7919u + it * 104729u) & n_mask;
         uint32_t idx;
         if (mode == 1) idx = (base & ~3u) | (lane % group & 3);       // same 32B sector (4 doubles)
+        else if (mode == 3) idx = (base & ~3u) | (lane & 3);          // group lanes in one sector, 4 addresses
         else idx = base;                                              // same address if mode 2
         atomicAdd(g + idx, (T)1);
     }
@@ -33,7 +34,8 @@ int main() {
     const double ops = (double)blocks * threads * iters;
     struct { int group, mode; const char* name; } cases[] = {
         {1, 0, "distinct addresses"}, {2, 1, "2 lanes per sector"}, {4, 1, "4 lanes per sector"},
-        {2, 2, "2 lanes per address"}, {8, 2, "8 lanes per address"}, {32, 2, "32 lanes per address"}};
+        {2, 2, "2 lanes per address"}, {8, 2, "8 lanes per address"}, {32, 2, "32 lanes per address"},
+        {8, 3, "8 lanes/sector, 4 addr"}, {32, 3, "32 lanes/sector, 4 addr"}};
     for (auto c : cases) {
         for (int f = 0; f < 2; ++f) {
             for (int rep = 0; rep < 2; ++rep) {
