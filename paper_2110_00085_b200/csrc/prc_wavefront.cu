@@ -45,7 +45,7 @@ constexpr int kTPB = 128;
 #define PRC_GRAD3_MINB 4
 #endif
 #ifndef PRC_GRAD4_MINB
-#define PRC_GRAD4_MINB 1
+#define PRC_GRAD4_MINB 3
 #endif
 constexpr int kFwdMinBlocks = PRC_FWD_MINB;
 
@@ -413,14 +413,32 @@ __global__ void __launch_bounds__(128, M == 2 ? PRC_GRAD2_MINB : (M == 3 ? PRC_G
                 const int v1 = dda_step_pad(S[1], l1);
                 const int v2 = dda_step_pad(S[2], l2);
                 const double x1 = cf[1] * l1, x2 = cf[2] * l2;
-                const bool s10 = v1 >= 0 && v1 == v0;
-                const bool s20 = v2 >= 0 && v2 == v0;
-                const bool s21 = v2 >= 0 && v2 == v1 && !s20;
+                // dead or zero-length emissions are -1: they only ever match each other,
+                // and emissions at -1 are suppressed, so no validity tests are needed
+                const bool s10 = v1 == v0;
+                const bool s20 = v2 == v0;
+                const bool s21 = v2 == v1 && !s20;
                 red_add_if(g, v0, cf[0] * l0 + (s10 ? x1 : 0.0) + (s20 ? x2 : 0.0));
                 red_add_if(g, s10 ? -1 : v1, x1 + (s21 ? x2 : 0.0));
                 red_add_if(g, (s20 || s21) ? -1 : v2, x2);
             };
             while (S[0].alive || S[1].alive || S[2].alive) step3();  // (unrolling x2 measured slower)
+        } else if (M == 4) {  // hand-scheduled quad
+            while (S[0].alive || S[1].alive || S[2].alive || S[3].alive) {
+                double l0, l1, l2, l3;
+                const int v0 = dda_step_pad(S[0], l0);
+                const int v1 = dda_step_pad(S[1], l1);
+                const int v2 = dda_step_pad(S[2], l2);
+                const int v3 = dda_step_pad(S[3], l3);
+                const double x1 = cf[1] * l1, x2 = cf[2] * l2, x3 = cf[3] * l3;
+                const bool s10 = v1 == v0, s20 = v2 == v0, s30 = v3 == v0;
+                const bool s21 = v2 == v1 && !s20, s31 = v3 == v1 && !s30;
+                const bool s32 = v3 == v2 && !s30 && !s31;
+                red_add_if(g, v0, cf[0] * l0 + (s10 ? x1 : 0.0) + (s20 ? x2 : 0.0) + (s30 ? x3 : 0.0));
+                red_add_if(g, s10 ? -1 : v1, x1 + (s21 ? x2 : 0.0) + (s31 ? x3 : 0.0));
+                red_add_if(g, (s20 || s21) ? -1 : v2, x2 + (s32 ? x3 : 0.0));
+                red_add_if(g, (s30 || s31 || s32) ? -1 : v3, x3);
+            }
         } else {
             bool any = false;
 #pragma unroll
