@@ -305,11 +305,17 @@ def cpu_baseline(cfg, scene, n_cpu=None):
     if ref is not None:
         st = ref.time_iteration(scene, None, tp, n, 7, cores, reps=3, warmup=1)
         secs = st["forward_s"] + st["grad_s"]
-        return {"value": st["segments"] / secs, "unit": "path-segments/s", "cores": cores,
-                "kind": kind, "sample": f"{n} paths of the same workload, traced then sorted; "
-                f"mean of 3 timed recycled_render + grad_forward iterations after 1 warm-up "
-                f"({secs:.2f} s each, {cores} threads)",
-                "forward_s": st["forward_s"], "grad_s": st["grad_s"]}
+        out = {"value": st["segments"] / secs, "unit": "path-segments/s", "cores": cores,
+               "kind": kind, "sample": f"{n} paths of the same workload, traced then sorted; "
+               f"mean of 3 timed recycled_render + grad_forward iterations after 1 warm-up "
+               f"({secs:.2f} s each, {cores} threads)",
+               "forward_s": st["forward_s"], "grad_s": st["grad_s"]}
+        if cores > 1:  # also the single-worker rate, on a smaller sample
+            n1 = max(1000, n // 8)
+            s1 = ref.time_iteration(scene, None, tp, n1, 7, 1, reps=1, warmup=0)
+            out["value_1thread"] = s1["segments"] / (s1["forward_s"] + s1["grad_s"])
+            out["sample_1thread"] = f"{n1} paths, 1 timed iteration, 1 thread"
+        return out
     port = pyoracle.Port()
     _, _, store = port.render(scene, n, 7)
     store.sort_by_size()
