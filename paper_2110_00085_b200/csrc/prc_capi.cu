@@ -108,7 +108,7 @@ struct prc_gpu_ctx {
     unsigned long long launches = 0;
     int mode = 0;        // 0: event-major wavefront (default), 1: fused thread-per-path
     bool timed_sub = false, timed_grad = false;  // sub-phase events recorded this call
-    int spread = 64;     // K5b lane spreading factor (packet 2: 8 best at 1e7, 64-128 at 1e8)
+    int spread = 64;     // K5b lane spreading factor (measured at 1e8: 64-128 best; 16 +10%, 1 +25%)
     int opt_per_species = 0;  // opt_step computes per-type gradients of every species
     int packet = 3;      // K5b rays per thread walked in lockstep (measured best: 3)
     bool pad_ok = false, pad_enable = true;  // guard-free padded walks valid / allowed

@@ -8,10 +8,13 @@
 //                       log-prefix at every interaction vertex -> lp[iv]
 //   K4b k_le_forward    CTA per run of Morton-ordered interaction vertices, camera by
 //                       camera: LE transmittance, event value, image scatter, event cache
-//   K5b k_le_gradient_ms<2>  same vertex order: w = value * residual, LE scatter -w*l
-//                       with fp64 L2 reductions (two rays per thread in lockstep, spans in
-//                       the same voxel merged in registers), vertex score terms,
+//   K5b k_le_gradient_ms<3>  same vertex order: w = value * residual, LE scatter -w*l
+//                       with fp64 L2 reductions (three rays per thread in lockstep, spans
+//                       in the same voxel merged in registers), vertex score terms,
 //                       per-vertex weight sums own[iv]
+//
+// The hot walks run guard-free over the padded voxel layout (prc_device.cuh, "guard-free
+// walks"): same spans as the reference walk plus a zero-beta border tail.
 //   K5a k_path_gradient thread per path: suffix sums from own[iv] -> incoming-segment
 //                       spans and continuation score terms
 //
@@ -334,7 +337,8 @@ __global__ void __launch_bounds__(kWF, PRC_GRAD1_MINB) k_le_gradient(const __gri
 // high vertex density they share a voxel) to the same camera in lockstep, one DDA step
 // per ray per iteration.  Spans that land in the same voxel at the same iteration are
 // summed in registers before a single fp64 L2 reduction, so the number of REDs falls
-// (~0.35 per voxel visit for M = 4 at 1e8 paths), while `spread` keeps the 32 lanes of a
+// (~0.39 per voxel visit for M = 3 at 1e8 paths: the reference DDA on the bench geometry
+// gives 0.53 / 0.39 / 0.31 for M = 2 / 3 / 4 vertices in a 0.3-voxel cube), while `spread` keeps the 32 lanes of a
 // warp on distinct packets far apart in Morton order (no same-address RED conflicts).
 template <int M>
 __global__ void __launch_bounds__(128, M == 2 ? PRC_GRAD2_MINB : (M == 3 ? PRC_GRAD3_MINB : PRC_GRAD4_MINB)) k_le_gradient_ms(const __grid_constant__ DScene sc,
