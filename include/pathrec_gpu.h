@@ -306,7 +306,7 @@ typedef struct {              /* Schedule (inverse.hpp:28-35) + ReconstructOptio
     int saturation_window;    /* default 20 */
     double saturation_rel_improvement;  /* default 0.01 */
     int checkpoint_every;     /* 0 disables checkpoints */
-    const char* checkpoint_dir;         /* NULL or "" disables checkpoints */
+    const char* checkpoint_dir;         /* NULL or "" disables checkpoints; rank 0 writes */
     int length_unit;          /* VGRD unit tag of the checkpoints (LengthUnit) */
     const prc_gpu_params* truth;        /* optional ground-truth unknowns for eps/delta */
 } prc_gpu_schedule;

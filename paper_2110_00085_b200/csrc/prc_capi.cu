@@ -1930,7 +1930,7 @@ PRC_EXPORT int prc_gpu_reconstruct_schedule(prc_gpu_ctx* ctx, const prc_gpu_para
         if (!truth.empty()) metrics_host(x_host.data(), truth.data(), truth.size(), &row.eps, &row.delta);
         rows.push_back(row);
         if (history) history[t] = row;
-        if (ckpt && (t + 1) % sch->checkpoint_every == 0) {
+        if (ckpt && ctx->rank == 0 && (t + 1) % sch->checkpoint_every == 0) {  // replicas agree: rank 0 writes
             const std::string dir(sch->checkpoint_dir);
             if (ctx->opt_mode == 0 && ctx->dsc.has_medium)
                 save_grid_host(dir + "/checkpoint_" + std::to_string(t) + ".vgrd", ctx->dsc.dims, ctx->dsc.gorg,
