@@ -209,6 +209,9 @@ class Reference:
         L.ref_metrics.argtypes = [_dp, _dp, C.c_uint64, _dp, _dp]
         L.ref_save_grid.argtypes = [C.c_char_p, _i32p, _dp, _dp, C.c_int, _dp]
         L.ref_save_csv.argtypes = [C.c_char_p, C.c_int, _i32p, _dp, _dp, _dp, _dp, _i32p]
+        L.ref_render_json.argtypes = [C.c_char_p, C.c_uint64, C.c_uint64, _dp, C.c_uint64]
+        L.ref_save_pfm.argtypes = [C.c_char_p, C.c_int, C.c_int, _dp]
+        L.ref_load_pfm.argtypes = [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int), _dp, C.c_uint64]
 
     def _err(self):
         return self.lib.ref_last_error().decode()
@@ -352,3 +355,23 @@ class Reference:
         cols = [np.ascontiguousarray(history[k], np.float64) for k in ("time_s", "loss", "eps", "delta")]
         if self.lib.ref_save_csv(path.encode(), n, _ptr(it, _i32p), *[_ptr(c, _dp) for c in cols], _ptr(st, _i32p)):
             raise ValueError(self._err())
+
+    def render_json(self, path: str, n: int, seed: int, n_pix: int) -> np.ndarray:
+        out = np.zeros(n_pix)
+        if self.lib.ref_render_json(path.encode(), n, seed, _ptr(out, _dp), n_pix):
+            raise ValueError(self._err())
+        return out
+
+    def save_pfm(self, path: str, image: np.ndarray):
+        im = np.ascontiguousarray(image, dtype=np.float64)
+        if self.lib.ref_save_pfm(path.encode(), im.shape[0], im.shape[1], _ptr(im, _dp)):
+            raise ValueError(self._err())
+
+    def load_pfm(self, path: str) -> np.ndarray:
+        r, c = C.c_int(), C.c_int()
+        if self.lib.ref_load_pfm(path.encode(), C.byref(r), C.byref(c), None, 0):
+            raise ValueError(self._err())
+        out = np.zeros(r.value * c.value)
+        if self.lib.ref_load_pfm(path.encode(), C.byref(r), C.byref(c), _ptr(out, _dp), out.size):
+            raise ValueError(self._err())
+        return out.reshape(r.value, c.value)

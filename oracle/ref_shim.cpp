@@ -433,4 +433,52 @@ int ref_save_csv(const char* path, int n, const int* iter, const double* time_s,
     }
 }
 
+/* load_scene (io.cpp:190-278) + render (transport.cpp:405-454): images of a JSON scene. */
+int ref_render_json(const char* path, uint64_t n, uint64_t seed, double* images, uint64_t cap) {
+    try {
+        Scene s = load_scene(path);
+        RenderOptions o;
+        o.n_paths = n;
+        o.seed = seed;
+        o.workers = 1;
+        RenderResult r = render(s, o);
+        size_t k = 0;
+        for (const auto& im : r.images)
+            for (double px : im.data) {
+                if (k >= cap) throw std::runtime_error("ref_render_json: capacity");
+                images[k++] = px;
+            }
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+/* save_pfm / load_pfm (io.cpp:94-129). */
+int ref_save_pfm(const char* path, int rows, int cols, const double* data) {
+    try {
+        Image im = Image::zeros(rows, cols);
+        for (size_t i = 0; i < im.data.size(); ++i) im.data[i] = data[i];
+        save_pfm(im, path);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int ref_load_pfm(const char* path, int* rows, int* cols, double* data, uint64_t cap) {
+    try {
+        Image im = load_pfm(path);
+        *rows = im.rows;
+        *cols = im.cols;
+        if (data) {
+            if (im.data.size() > cap) throw std::runtime_error("ref_load_pfm: capacity");
+            for (size_t i = 0; i < im.data.size(); ++i) data[i] = im.data[i];
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
 }  // extern "C"

@@ -94,6 +94,7 @@ class Scene:
     surfaces: List[Surface] = field(default_factory=list)
     light: Light = field(default_factory=Light)
     detectors: List[Detector] = field(default_factory=list)
+    unit: int = 0  # LengthUnit tag (0 m, 1 km): informational, carried into VGRD checkpoints
 
     @property
     def voxel_count(self) -> int:
