@@ -48,9 +48,9 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str = OUT
             raise RuntimeError(f"nvcc failed on {s}")
         if verbose:
             sys.stderr.write(r.stderr)
-        if not tag:
+        if not tag:  # register / spill report (compile times dropped: the file is tracked)
             with open(os.path.join(SRC, s.replace(".cu", ".ptxas.txt")), "w") as f:
-                f.write(r.stderr)
+                f.write("".join(l for l in r.stderr.splitlines(True) if "Compile time" not in l))
         objs.append(obj)
     tmp = out + ".tmp"
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs,
