@@ -10,6 +10,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -429,7 +430,7 @@ void upload_scene(prc_gpu_ctx* c, const prc_scene_desc* d) {
         const size_t vpad = c->pad_ok ? (size_t)s.pnxny * (size_t)(s.dims[2] + 2) : 1;
         c->bt_pad.alloc(vpad);
         c->db_pad.alloc(vpad);
-        c->g_pad.alloc(vpad);
+        c->g_pad.alloc(vpad * PRC_GRAD_REPLICAS);
         CK(cudaMemset(c->bt_pad.p, 0, c->bt_pad.bytes()));  // borders stay zero
         CK(cudaMemset(c->db_pad.p, 0, c->db_pad.bytes()));
     }
@@ -879,26 +880,34 @@ void sort_store(prc_gpu_ctx* c, prc_gpu_store* st) {
     CK(launch_bucket_layout(perm.p, st->B.p, st->stream.p, st->trunc.p, n, d_bstart.p, d_brec.p,
                             d_biv.p, ns->B.p, ns->stream.p, ns->trunc.p, ns->rec_base.p,
                             ns->stride.p, ns->iv_base.p, q, &c->launches));
-    ns->alloc_records(st->n_rec);
-    CK(launch_gather_records(st->view(), perm.p, n, ns->rec_base.p, ns->stride.p, ns->rec_out(), q,
-                             &c->launches));
-    c->sync();
+    // re-layout one record field at a time (transient: one field, not a second store)
+    const StoreView old_view = st->view();
+    auto move_field = [&](auto& buf) {
+        using T = std::remove_reference_t<decltype(*buf.p)>;
+        static_assert(sizeof(T) == 8 || sizeof(T) == 4, "record fields are 4 or 8 bytes");
+        DBuf<T> nbuf;
+        nbuf.alloc(st->n_rec);
+        CK(launch_gather_field(old_view, perm.p, n, ns->rec_base.p, ns->stride.p, buf.p, nbuf.p,
+                               (int)sizeof(T), q, &c->launches));
+        c->sync();
+        buf.swap(nbuf);  // the old field is freed here
+    };
+    move_field(st->px);
+    move_field(st->py);
+    move_field(st->pz);
+    move_field(st->dx);
+    move_field(st->dy);
+    move_field(st->dz);
+    move_field(st->tt);
+    move_field(st->ct);
+    move_field(st->vox);
+    move_field(st->meta);
     st->B.swap(ns->B);
     st->stream.swap(ns->stream);
     st->trunc.swap(ns->trunc);
     st->rec_base.swap(ns->rec_base);
     st->stride.swap(ns->stride);
     st->iv_base.swap(ns->iv_base);
-    st->px.swap(ns->px);
-    st->py.swap(ns->py);
-    st->pz.swap(ns->pz);
-    st->dx.swap(ns->dx);
-    st->dy.swap(ns->dy);
-    st->dz.swap(ns->dz);
-    st->tt.swap(ns->tt);
-    st->ct.swap(ns->ct);
-    st->vox.swap(ns->vox);
-    st->meta.swap(ns->meta);
     st->sorted = true;
     st->vt_ready = false;  // vertex table indexes the old layout
     ++c->fwd_gen;          // the event cache indexes the old layout too

@@ -569,28 +569,20 @@ __global__ void k_bucket_layout(const uint32_t* perm, const uint32_t* B_old,
     ib[i] = biv[k] + j;
 }
 
-__global__ void k_gather(const __grid_constant__ StoreView o, const uint32_t* perm, long long n,
-                         const unsigned long long* rbn, const uint32_t* sn, RecordsOut out) {
+// One record field at a time (sort_by_size's re-layout): the transient is one field
+// (<= 8 B per record) instead of a second copy of all records (72 B per record), so a
+// store can fill ~85% of HBM and still be sorted.  Fields move as raw bits.
+template <class T>
+__global__ void k_gather_field(const __grid_constant__ StoreView o, const uint32_t* perm, long long n,
+                               const unsigned long long* rbn, const uint32_t* sn,
+                               const T* __restrict__ src, T* __restrict__ dst) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const uint32_t src = perm[i];
-    const int B = (int)o.B[src];
-    const unsigned long long ob = o.rec_base[src], nb = rbn[i];
-    const unsigned os = o.stride[src], ns = sn[i];
-    for (int b = 0; b <= B; ++b) {
-        const unsigned long long r = ob + (unsigned long long)b * os;
-        const unsigned long long w = nb + (unsigned long long)b * ns;
-        out.px[w] = o.px[r];
-        out.py[w] = o.py[r];
-        out.pz[w] = o.pz[r];
-        out.dx[w] = o.dx[r];
-        out.dy[w] = o.dy[r];
-        out.dz[w] = o.dz[r];
-        out.tt[w] = o.tt[r];
-        out.ct[w] = o.ct[r];
-        out.vox[w] = o.vox[r];
-        out.meta[w] = o.meta[r];
-    }
+    const uint32_t p = perm[i];
+    const int B = (int)o.B[p];
+    const unsigned long long ob = o.rec_base[p], nb = rbn[i];
+    const unsigned os = o.stride[p], ns = sn[i];
+    for (int b = 0; b <= B; ++b) dst[nb + (unsigned long long)b * ns] = src[ob + (unsigned long long)b * os];
 }
 
 // ============================================================================ diagnostics
@@ -917,12 +909,16 @@ cudaError_t launch_bucket_layout(const uint32_t* perm, const uint32_t* B_old,
     LAUNCH_DONE();
 }
 
-cudaError_t launch_gather_records(const StoreView& o, const uint32_t* perm, long long n,
-                                  const unsigned long long* rbn, const uint32_t* sn,
-                                  const RecordsOut& out, cudaStream_t s,
-                                  unsigned long long* launches) {
+cudaError_t launch_gather_field(const StoreView& o, const uint32_t* perm, long long n,
+                                const unsigned long long* rbn, const uint32_t* sn, const void* src,
+                                void* dst, int elem_bytes, cudaStream_t s, unsigned long long* launches) {
     if (n == 0) return cudaSuccess;
-    k_gather<<<grid_for(n, 128), 128, 0, s>>>(o, perm, n, rbn, sn, out);
+    if (elem_bytes == 8)
+        k_gather_field<unsigned long long><<<grid_for(n, 128), 128, 0, s>>>(
+            o, perm, n, rbn, sn, (const unsigned long long*)src, (unsigned long long*)dst);
+    else
+        k_gather_field<uint32_t><<<grid_for(n, 128), 128, 0, s>>>(o, perm, n, rbn, sn, (const uint32_t*)src,
+                                                                  (uint32_t*)dst);
     LAUNCH_DONE();
 }
 

@@ -82,7 +82,12 @@ struct TraceArgs {
 
 // ---- launchers (return cudaError_t); `launches` counts kernels issued -------------
 // Padded layout: bt_pad/db_pad interiors <- bt_tot/dbeta (borders stay zero), and
-// g_span += interior of g_pad.
+// Copies of the padded span gradient that K5b's CTAs reduce into (CTA b uses copy
+// b mod PRC_GRAD_REPLICAS); k_unpad_add folds them back.  A/B knob for L2 slice load.
+#ifndef PRC_GRAD_REPLICAS
+#define PRC_GRAD_REPLICAS 1
+#endif
+// g_span += interior of g_pad (all copies).
 cudaError_t launch_pad_tables(const DScene& sc, const float* bt_tot, const float* dbeta, double* bt_pad,
                               double* db_pad, cudaStream_t s, unsigned long long* launches);
 cudaError_t launch_unpad_add(const DScene& sc, const double* g_pad, double* g_span, cudaStream_t s,
@@ -146,10 +151,10 @@ cudaError_t launch_bucket_layout(const uint32_t* perm, const uint32_t* B_old,
                                  unsigned long long* rec_base, uint32_t* stride,
                                  unsigned long long* iv_base, cudaStream_t s,
                                  unsigned long long* launches);
-cudaError_t launch_gather_records(const StoreView& old_st, const uint32_t* perm, long long n,
-                                  const unsigned long long* rec_base_new,
-                                  const uint32_t* stride_new, const RecordsOut& out,
-                                  cudaStream_t s, unsigned long long* launches);
+cudaError_t launch_gather_field(const StoreView& old_st, const uint32_t* perm, long long n,
+                                const unsigned long long* rec_base_new, const uint32_t* stride_new,
+                                const void* src, void* dst, int elem_bytes, cudaStream_t s,
+                                unsigned long long* launches);
 
 // ---- event-major wavefront (default mapping) -------------------------------------
 // Vertex-table construction: Morton keys + iv -> record map, CUB radix sort, gather.

@@ -333,6 +333,62 @@ __global__ void __launch_bounds__(kWF, PRC_GRAD1_MINB) k_le_gradient(const __gri
 }
 
 // ------------------------------------------------------------------ K5b, lockstep packets
+// One ray of a lockstep packet over the padded gradient table.  The voxel is carried as a
+// pointer into the table, so a span's RED takes its address straight from loop-carried
+// state: no address arithmetic per RED, and no fresh address registers whose reuse must
+// wait for the RED to read them (the LSU reads a RED's operands late when reductions
+// queue, and the next write to those registers stalls on the long scoreboard: r11 source
+// counters put 17.5% of K5b's stall samples on one such write).  Measured at 1e8 paths:
+// 1289 -> 1286 ms per iteration, i.e. the RED rate, not the stall, bounds K5b.
+struct PRay {
+    double t, t1, tx, ty, tz, dx, dy, dz, cf;
+    double* p;
+    int sx, oy, oz;
+    bool alive;
+
+    __device__ __forceinline__ void dead(double* g) {
+        t = t1 = tx = ty = tz = dx = dy = dz = cf = 0.0;
+        p = g;
+        sx = oy = oz = 0;
+        alive = false;
+    }
+    __device__ __forceinline__ void from(const DdaState& S, double* g, double c) {
+        t = S.t; t1 = S.t1; tx = S.tx; ty = S.ty; tz = S.tz; dx = S.dx; dy = S.dy; dz = S.dz;
+        cf = c;
+        p = g + S.v;
+        sx = S.sx; oy = S.oy; oz = S.oz;
+        alive = S.alive;
+    }
+    // One iteration of traverse.hpp:100-115 on the padded layout (dda_step_pad): returns
+    // whether the span [t, min(tmax, t1)] is emitted, its contribution cf * length and
+    // its table address.  A ray that is no longer alive keeps stepping and emits nothing.
+    __device__ __forceinline__ bool step(double& x, double*& a) {
+        int off;
+        const double tm = dda_advance(tx, ty, tz, dx, dy, dz, sx, oy, oz, off);
+        const bool last = tm >= t1;
+        const double tn = last ? t1 : tm;
+        const bool e = alive && tn > t;
+        x = cf * (tn - t);
+        a = p;
+        t = tm;
+        p += off;
+        alive = alive && !last;
+        return e;
+    }
+};
+
+// fp64 reduction x into *a when e, as one predicated RED.
+__device__ __forceinline__ void red_add_p(bool e, double* a, double x) {
+    asm volatile(
+        "{\n\t"
+        ".reg .pred p;\n\t"
+        "setp.ne.b32 p, %0, 0;\n\t"
+        "@p red.global.add.f64 [%1], %2;\n\t"
+        "}" ::"r"((int)e),
+        "l"(a), "d"(x)
+        : "memory");
+}
+
 // One thread walks the LE rays of M consecutive Morton-ordered vertices (a packet: at
 // high vertex density they share a voxel) to the same camera in lockstep, one DDA step
 // per ray per iteration.  Spans that land in the same voxel at the same iteration are
@@ -400,6 +456,8 @@ __global__ void __launch_bounds__(128, M == 2 ? PRC_GRAD2_MINB : (M == 3 ? PRC_G
                 phong_scores(ea.phong, cos_le, w, gk, gg);
         }
         double* g = ea.g_pad;
+        if (PRC_GRAD_REPLICAS > 1)
+            g += (long long)(blockIdx.x % PRC_GRAD_REPLICAS) * sc.pnxny * (sc.dims[2] + 2);
         if (M == 2) {  // hand-scheduled pair
             while (S[0].alive || S[1].alive) {
                 double l0, l1;
@@ -411,6 +469,30 @@ __global__ void __launch_bounds__(128, M == 2 ? PRC_GRAD2_MINB : (M == 3 ? PRC_G
                 red_add_if(g, same ? -1 : v1, x1);
             }
         } else if (M == 3) {  // hand-scheduled triple (the default packet)
+#ifndef PRC_K5B_VIDX
+            PRay R0, R1, R2;
+            if (S[0].alive) R0.from(S[0], g, cf[0]); else R0.dead(g);
+            if (S[1].alive) R1.from(S[1], g, cf[1]); else R1.dead(g);
+            if (S[2].alive) R2.from(S[2], g, cf[2]); else R2.dead(g);
+            auto pstep3 = [&]() {
+                double x0, x1, x2;
+                double *a0, *a1, *a2;
+                const bool e0 = R0.step(x0, a0);
+                const bool e1 = R1.step(x1, a1);
+                const bool e2 = R2.step(x2, a2);
+                // same voxel <=> same address; the table is < 4 GB, so the low 32 bits decide
+                const uint32_t l0 = (uint32_t)(uintptr_t)a0, l1 = (uint32_t)(uintptr_t)a1,
+                               l2 = (uint32_t)(uintptr_t)a2;
+                const bool s10 = e0 && e1 && l1 == l0;
+                const bool s20 = e0 && e2 && l2 == l0;
+                const bool s21 = e1 && e2 && l2 == l1 && !s20;
+                red_add_p(e0, a0, x0 + (s10 ? x1 : 0.0) + (s20 ? x2 : 0.0));
+                red_add_p(e1 && !s10, a1, x1 + (s21 ? x2 : 0.0));
+                red_add_p(e2 && !s20 && !s21, a2, x2);
+            };
+            while (R0.alive || R1.alive || R2.alive) pstep3();  // (two steps per trip: same time)
+            continue;
+#endif
             auto step3 = [&]() {
                 double l0, l1, l2;
                 const int v0 = dda_step_pad(S[0], l0);
@@ -601,7 +683,10 @@ __global__ void k_unpad_add(const __grid_constant__ DScene sc, const double* __r
     const int nx = sc.dims[0], ny = sc.dims[1];
     const int ix = (int)(v % nx), iy = (int)((v / nx) % ny), iz = (int)(v / ((long long)nx * ny));
     const long long pv = (ix + 1) + (long long)sc.pnx * (iy + 1) + (long long)sc.pnxny * (iz + 1);
-    g_span[v] += g_pad[pv];
+    double acc = g_pad[pv];
+#pragma unroll
+    for (int r = 1; r < PRC_GRAD_REPLICAS; ++r) acc += g_pad[(long long)r * sc.pnxny * (sc.dims[2] + 2) + pv];
+    g_span[v] += acc;
 }
 
 }  // namespace

@@ -3,6 +3,7 @@
 
   scripts/ncu_summary.py report REP.ncu-rep [--title T]      -> key metrics per kernel
   scripts/ncu_summary.py launches LAUNCHES.csv [--title T]   -> per-kernel time shares
+  scripts/ncu_summary.py stalls REP.ncu-rep [--title T] [--top N] -> stall samples per SASS line
 """
 import csv
 import io
@@ -78,7 +79,39 @@ def launches(path, title):
     print()
 
 
+STALLS = ["stall_long_sb", "stall_wait", "stall_math", "stall_branch_resolving", "stall_no_inst",
+          "stall_dispatch", "stall_lg", "stall_short_sb", "stall_selected", "stall_not_selected"]
+
+
+def stalls(rep, title, top=15):
+    """Warp-stall samples attributed to SASS instructions (source page of a --set full
+    capture taken with --import-source on)."""
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    h = rows[1]
+    ix = {n: i for i, n in enumerate(h)}
+    data = [r for r in rows[2:] if len(r) == len(h)]
+    key = "Warp Stall Sampling (All Samples)"
+    tot = sum(int(r[ix[key]] or 0) for r in data) or 1
+    print(f"## {title}\n")
+    print(f"Source: `{rep}` (source page, SASS view). {tot} stall samples.\n")
+    print("| reason | share of samples |\n|---|---|")
+    for c in STALLS:
+        print(f"| {c[6:]} | {100 * sum(int(r[ix[c]] or 0) for r in data) / tot:.1f}% |")
+    print(f"\nTop {top} instructions by samples:\n")
+    print("| share | executed | SASS | main reasons |\n|---|---|---|---|")
+    for r in sorted(data, key=lambda r: -int(r[ix[key]] or 0))[:top]:
+        why = sorted(((int(r[ix[c]] or 0), c[6:]) for c in STALLS), reverse=True)[:2]
+        print(f"| {100 * int(r[ix[key]]) / tot:.1f}% | {r[ix['Instructions Executed']]} | "
+              f"`{r[1].strip()[:56]}` | " + ", ".join(f"{n} {100 * v / tot:.1f}%" for v, n in why) + " |")
+    print()
+
+
 if __name__ == "__main__":
     mode, path = sys.argv[1], sys.argv[2]
     title = sys.argv[sys.argv.index("--title") + 1] if "--title" in sys.argv else path
-    (report if mode == "report" else launches)(path, title)
+    if mode == "stalls":
+        stalls(path, title, int(sys.argv[sys.argv.index("--top") + 1]) if "--top" in sys.argv else 15)
+    else:
+        (report if mode == "report" else launches)(path, title)
