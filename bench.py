@@ -186,6 +186,8 @@ def run_ours(args):
         ctx.set_option("spread", args.spread)
     if args.packet is not None:
         ctx.set_option("packet", args.packet)
+    if args.grad_copies is not None:
+        ctx.set_option("grad_copies", args.grad_copies)
     ctx.upload(scene)
     t0 = time.time()
     rr = ctx.render(scene, RenderOptions(n_paths=n_paths, seed=7, keep_paths=True,
@@ -234,7 +236,7 @@ def run_ours(args):
     bytes_pass = 8.0 * W_live + 64.0 * vert_global + 16.0 * E
     bytes_iter = 2.0 * bytes_pass
     peak, peak_kind = measured_peak()
-    # Dominant kernel (launch list: profiles/r10_kernels_1e8.md): K5b, the LE-ray gradient
+    # Dominant kernel (launch list: profiles/r11_kernels_1e8.md): K5b, the LE-ray gradient
     # scatter.  Its event-timed duration is the gradient phase minus K5a (+ the padded
     # fold), and its algorithmic bytes are the §8(d) per-unit figures over the units it
     # processes: 8 B per LE span incidence, 16 B per event, 64 B per vertex.
@@ -391,6 +393,7 @@ def main():
     ap.add_argument("--mode", type=int, default=None, help="0 wavefront (default), 1 fused per-path")
     ap.add_argument("--spread", type=int, default=None, help="K5b lane spreading factor")
     ap.add_argument("--packet", type=int, default=None, help="K5b rays per thread in lockstep")
+    ap.add_argument("--grad-copies", type=int, default=None, help="max copies of the padded gradient K5b reduces into")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

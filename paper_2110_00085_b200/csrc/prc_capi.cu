@@ -150,6 +150,8 @@ struct prc_gpu_ctx {
     cudaEvent_t ev[9] = {};  // [0..5] phases, [6] after K4a, [7] before K5a, [8] spare
     cudaEvent_t timer[2] = {};
     double last_ms[8] = {};
+    int g_pad_copies = 1;  // see EvalArgs::g_pad_copies
+    int grad_copies_max = 0;  // option "grad_copies" (applied at scene upload); 0: 4
     ~prc_gpu_ctx() {
         if (cub_tmp) cudaFree(cub_tmp);
         for (auto& e : timer)
@@ -430,7 +432,12 @@ void upload_scene(prc_gpu_ctx* c, const prc_scene_desc* d) {
         const size_t vpad = c->pad_ok ? (size_t)s.pnxny * (size_t)(s.dims[2] + 2) : 1;
         c->bt_pad.alloc(vpad);
         c->db_pad.alloc(vpad);
-        c->g_pad.alloc(vpad * PRC_GRAD_REPLICAS);
+        // copies of the padded gradient for K5b (EvalArgs::g_pad_copies): as many as fit in
+        // 80 MB (4 at 128^3, 1 at 256^3 where one copy already exceeds L2), at most 4
+        const size_t cap = c->grad_copies_max > 0 ? (size_t)c->grad_copies_max : 4;
+        c->g_pad_copies =
+            c->pad_ok && vpad > 0 ? (int)std::max<size_t>(1, std::min<size_t>(cap, (80u << 20) / (vpad * 8))) : 1;
+        c->g_pad.alloc(vpad * (size_t)c->g_pad_copies);
         CK(cudaMemset(c->bt_pad.p, 0, c->bt_pad.bytes()));  // borders stay zero
         CK(cudaMemset(c->db_pad.p, 0, c->db_pad.bytes()));
     }
@@ -597,6 +604,8 @@ EvalArgs eval_args(prc_gpu_ctx* c, prc_gpu_store* st, const EvalRun& er, const d
     ea.bt_pad = c->bt_pad.p;
     ea.db_pad = c->db_pad.p;
     ea.g_pad = c->g_pad.p;
+    ea.g_pad_copies = c->g_pad_copies;
+    ea.g_pad_stride = (long long)(c->g_pad.n / (size_t)std::max(1, c->g_pad_copies));
     ea.g_vert = c->g_vert.p;
     ea.g_phong = c->g_phong.p;
     ea.per_species = er.per_species ? 1 : 0;
@@ -661,7 +670,7 @@ void run_gradient(prc_gpu_ctx* c, prc_gpu_store* st, const EvalArgs& ea) {
         CK(cudaEventRecord(c->ev[7], q));
         c->timed_grad = true;
         CK(launch_path_gradient(s, st->view(), ea, st->own.p, q, &c->launches));
-        if (s.pad_walk) CK(launch_unpad_add(s, c->g_pad.p, c->g_span.p, q, &c->launches));
+        if (s.pad_walk) CK(launch_unpad_add(s, c->g_pad.p, c->g_pad_copies, ea.g_pad_stride, c->g_span.p, q, &c->launches));
     } else {
         CK(launch_gradient(s, st->view(), ea, q, &c->launches));
     }
@@ -1347,6 +1356,9 @@ PRC_EXPORT int prc_gpu_ctx_set_option(prc_gpu_ctx* ctx, const char* key, int64_t
     } else if (k == "packet") {
         if (value < 1 || value > 4) return fail(PRC_ERR_CONFIG, "packet must be in 1..4");
         ctx->packet = (int)value;
+    } else if (k == "grad_copies") {
+        if (value < 0 || value > 64) return fail(PRC_ERR_CONFIG, "grad_copies must be in 0..64");
+        ctx->grad_copies_max = (int)value;
     } else if (k == "pad") {
         ctx->pad_enable = value != 0;
         ctx->dsc.pad_walk = ctx->pad_ok && ctx->pad_enable ? 1 : 0;

@@ -65,6 +65,12 @@ struct EvalArgs {
     const double* bt_pad;  // fp64: the walk's FMA takes it without an F2F conversion
     const double* db_pad;
     double* g_pad;
+    // K5b reduces into g_pad_copies copies of the padded gradient, g_pad_stride apart (CTA b
+    // into copy b mod copies): same-address reductions from many SMs spread over more L2
+    // lines.  Measured at 1e8 paths (config (b)): K5b 784 -> 718 ms with 2 copies, 697 with 4,
+    // 694 with 8.  k_unpad_add sums the copies; K5a uses copy 0.
+    long long g_pad_stride;
+    int g_pad_copies;
     int per_species, legacy, do_beta;
 };
 
@@ -82,15 +88,11 @@ struct TraceArgs {
 
 // ---- launchers (return cudaError_t); `launches` counts kernels issued -------------
 // Padded layout: bt_pad/db_pad interiors <- bt_tot/dbeta (borders stay zero), and
-// Copies of the padded span gradient that K5b's CTAs reduce into (CTA b uses copy
-// b mod PRC_GRAD_REPLICAS); k_unpad_add folds them back.  A/B knob for L2 slice load.
-#ifndef PRC_GRAD_REPLICAS
-#define PRC_GRAD_REPLICAS 1
-#endif
 // g_span += interior of g_pad (all copies).
 cudaError_t launch_pad_tables(const DScene& sc, const float* bt_tot, const float* dbeta, double* bt_pad,
                               double* db_pad, cudaStream_t s, unsigned long long* launches);
-cudaError_t launch_unpad_add(const DScene& sc, const double* g_pad, double* g_span, cudaStream_t s,
+cudaError_t launch_unpad_add(const DScene& sc, const double* g_pad, int copies, long long stride,
+                             double* g_span, cudaStream_t s,
                              unsigned long long* launches);
 cudaError_t launch_trace(const DScene& sc, const TraceArgs& a, bool write, cudaStream_t s,
                          unsigned long long* launches);

@@ -414,7 +414,15 @@ __global__ void __launch_bounds__(128, M == 2 ? PRC_GRAD2_MINB : (M == 3 ? PRC_G
 #pragma unroll
     for (int r = 0; r < M; ++r) own_acc[r] = acc[r] = 0.0;
     double gk = 0.0, gg = 0.0;
+#ifdef PRC_CAM_ROTATE
+    // CTAs start at different cameras, so concurrently resident CTAs reduce along
+    // different camera pencils (fewer same-line reductions across SMs)
+    const int rot = (int)(blockIdx.x % (unsigned)sc.n_det);
+    for (int kk = 0; kk < sc.n_det; ++kk) {
+        const int k = kk + rot < sc.n_det ? kk + rot : kk + rot - sc.n_det;
+#else
     for (int k = 0; k < sc.n_det; ++k) {
+#endif
         DdaState S[M];
         double cf[M];
 #pragma unroll
@@ -456,8 +464,7 @@ __global__ void __launch_bounds__(128, M == 2 ? PRC_GRAD2_MINB : (M == 3 ? PRC_G
                 phong_scores(ea.phong, cos_le, w, gk, gg);
         }
         double* g = ea.g_pad;
-        if (PRC_GRAD_REPLICAS > 1)
-            g += (long long)(blockIdx.x % PRC_GRAD_REPLICAS) * sc.pnxny * (sc.dims[2] + 2);
+        if (ea.g_pad_copies > 1) g += (long long)(blockIdx.x % ea.g_pad_copies) * ea.g_pad_stride;
         if (M == 2) {  // hand-scheduled pair
             while (S[0].alive || S[1].alive) {
                 double l0, l1;
@@ -677,15 +684,14 @@ __global__ void k_pad_tables(const __grid_constant__ DScene sc, const float* __r
 }
 
 __global__ void k_unpad_add(const __grid_constant__ DScene sc, const double* __restrict__ g_pad,
-                            double* __restrict__ g_span) {
+                            int copies, long long stride, double* __restrict__ g_span) {
     const long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= sc.V) return;
     const int nx = sc.dims[0], ny = sc.dims[1];
     const int ix = (int)(v % nx), iy = (int)((v / nx) % ny), iz = (int)(v / ((long long)nx * ny));
     const long long pv = (ix + 1) + (long long)sc.pnx * (iy + 1) + (long long)sc.pnxny * (iz + 1);
     double acc = g_pad[pv];
-#pragma unroll
-    for (int r = 1; r < PRC_GRAD_REPLICAS; ++r) acc += g_pad[(long long)r * sc.pnxny * (sc.dims[2] + 2) + pv];
+    for (int r = 1; r < copies; ++r) acc += g_pad[(long long)r * stride + pv];
     g_span[v] += acc;
 }
 
@@ -779,9 +785,9 @@ cudaError_t launch_pad_tables(const DScene& sc, const float* bt_tot, const float
     LAUNCH_DONE();
 }
 
-cudaError_t launch_unpad_add(const DScene& sc, const double* g_pad, double* g_span, cudaStream_t s,
-                             unsigned long long* launches) {
+cudaError_t launch_unpad_add(const DScene& sc, const double* g_pad, int copies, long long stride,
+                             double* g_span, cudaStream_t s, unsigned long long* launches) {
     if (sc.V == 0) return cudaSuccess;
-    k_unpad_add<<<grid_for(sc.V, 256), 256, 0, s>>>(sc, g_pad, g_span);
+    k_unpad_add<<<grid_for(sc.V, 256), 256, 0, s>>>(sc, g_pad, copies, stride, g_span);
     LAUNCH_DONE();
 }
