@@ -414,15 +414,7 @@ __global__ void __launch_bounds__(128, M == 2 ? PRC_GRAD2_MINB : (M == 3 ? PRC_G
 #pragma unroll
     for (int r = 0; r < M; ++r) own_acc[r] = acc[r] = 0.0;
     double gk = 0.0, gg = 0.0;
-#ifdef PRC_CAM_ROTATE
-    // CTAs start at different cameras, so concurrently resident CTAs reduce along
-    // different camera pencils (fewer same-line reductions across SMs)
-    const int rot = (int)(blockIdx.x % (unsigned)sc.n_det);
-    for (int kk = 0; kk < sc.n_det; ++kk) {
-        const int k = kk + rot < sc.n_det ? kk + rot : kk + rot - sc.n_det;
-#else
     for (int k = 0; k < sc.n_det; ++k) {
-#endif
         DdaState S[M];
         double cf[M];
 #pragma unroll
