@@ -10,7 +10,6 @@
 #include <nccl.h>
 
 #include <algorithm>
-#include <type_traits>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -758,14 +757,7 @@ std::unique_ptr<prc_gpu_store> trace_store(prc_gpu_ctx* c, const prc_gpu_render_
     st->trunc.alloc(std::max<unsigned long long>(n, 1));
     st->stream.alloc(std::max<unsigned long long>(n, 1));
     // stream ids of a fresh shard are stream_base + i
-    {
-        std::vector<unsigned long long> ids(n);
-        for (unsigned long long i = 0; i < n; ++i) ids[i] = st->stream_base + i;
-        if (n)
-            CK(cudaMemcpyAsync(st->stream.p, ids.data(), n * sizeof(unsigned long long),
-                               cudaMemcpyHostToDevice, q));
-        c->sync();
-    }
+    CK(launch_iota_u64(st->stream.p, (long long)n, st->stream_base, q, &c->launches));
     TraceArgs a{};
     a.beta_tot = st->br_tot64.p;
     a.sp_beta = sp_dev;
@@ -823,11 +815,11 @@ std::unique_ptr<prc_gpu_store> trace_store(prc_gpu_ctx* c, const prc_gpu_render_
     CK(launch_trace(s, a, true, q, &c->launches));
     // truncated count
     {
-        std::vector<uint8_t> tr(n);
-        if (n) CK(cudaMemcpyAsync(tr.data(), st->trunc.p, n, cudaMemcpyDeviceToHost, q));
-        c->sync();
+        CK(cudaMemsetAsync(c->u64tmp_a.p, 0, sizeof(unsigned long long), q));
+        CK(launch_count_nonzero_u8(st->trunc.p, (long long)n, c->u64tmp_a.p, q, &c->launches));
         unsigned long long cnt = 0;
-        for (auto t : tr) cnt += t;
+        CK(cudaMemcpyAsync(&cnt, c->u64tmp_a.p, sizeof cnt, cudaMemcpyDeviceToHost, q));
+        c->sync();
         st->truncated = cnt;
     }
     return st;
@@ -889,28 +881,27 @@ void sort_store(prc_gpu_ctx* c, prc_gpu_store* st) {
     CK(launch_bucket_layout(perm.p, st->B.p, st->stream.p, st->trunc.p, n, d_bstart.p, d_brec.p,
                             d_biv.p, ns->B.p, ns->stream.p, ns->trunc.p, ns->rec_base.p,
                             ns->stride.p, ns->iv_base.p, q, &c->launches));
-    // re-layout one record field at a time (transient: one field, not a second store)
+    // re-layout one record field at a time through one spare field buffer (8 B per record,
+    // not a second store): an 8-byte field is gathered into the spare, which then takes the
+    // old field's place; the two 4-byte fields are gathered into the spare's halves and
+    // copied back
     const StoreView old_view = st->view();
-    auto move_field = [&](auto& buf) {
-        using T = std::remove_reference_t<decltype(*buf.p)>;
-        static_assert(sizeof(T) == 8 || sizeof(T) == 4, "record fields are 4 or 8 bytes");
-        DBuf<T> nbuf;
-        nbuf.alloc(st->n_rec);
-        CK(launch_gather_field(old_view, perm.p, n, ns->rec_base.p, ns->stride.p, buf.p, nbuf.p,
-                               (int)sizeof(T), q, &c->launches));
-        c->sync();
-        buf.swap(nbuf);  // the old field is freed here
-    };
-    move_field(st->px);
-    move_field(st->py);
-    move_field(st->pz);
-    move_field(st->dx);
-    move_field(st->dy);
-    move_field(st->dz);
-    move_field(st->tt);
-    move_field(st->ct);
-    move_field(st->vox);
-    move_field(st->meta);
+    DBuf<double> spare;
+    spare.alloc(st->n_rec);
+    for (DBuf<double>* f : {&st->px, &st->py, &st->pz, &st->dx, &st->dy, &st->dz, &st->tt, &st->ct}) {
+        CK(launch_gather_field(old_view, perm.p, n, ns->rec_base.p, ns->stride.p, f->p, spare.p, 8, q,
+                               &c->launches));
+        f->swap(spare);
+    }
+    uint32_t* half0 = reinterpret_cast<uint32_t*>(spare.p);
+    uint32_t* half1 = half0 + st->n_rec;
+    CK(launch_gather_field(old_view, perm.p, n, ns->rec_base.p, ns->stride.p, st->vox.p, half0, 4, q,
+                           &c->launches));
+    CK(launch_gather_field(old_view, perm.p, n, ns->rec_base.p, ns->stride.p, st->meta.p, half1, 4, q,
+                           &c->launches));
+    CK(cudaMemcpyAsync(st->vox.p, half0, st->n_rec * 4, cudaMemcpyDeviceToDevice, q));
+    CK(cudaMemcpyAsync(st->meta.p, half1, st->n_rec * 4, cudaMemcpyDeviceToDevice, q));
+    c->sync();
     st->B.swap(ns->B);
     st->stream.swap(ns->stream);
     st->trunc.swap(ns->trunc);

@@ -569,6 +569,19 @@ __global__ void k_bucket_layout(const uint32_t* perm, const uint32_t* B_old,
     ib[i] = biv[k] + j;
 }
 
+// Stream ids of a fresh shard (stream_base + i) and the truncated-path count, on the
+// device: at 1e8 paths the host versions moved 800 MB up and 100 MB down per resample.
+__global__ void k_iota_u64(unsigned long long* out, long long n, unsigned long long base) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = base + (unsigned long long)i;
+}
+
+__global__ void k_count_nonzero_u8(const uint8_t* x, long long n, unsigned long long* count) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const unsigned c = __popc(__ballot_sync(0xffffffffu, i < n && x[i] != 0));
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, (unsigned long long)c);
+}
+
 // One record field at a time (sort_by_size's re-layout): the transient is one field
 // (<= 8 B per record) instead of a second copy of all records (72 B per record), so a
 // store can fill ~85% of HBM and still be sorted.  Fields move as raw bits.
@@ -906,6 +919,20 @@ cudaError_t launch_bucket_layout(const uint32_t* perm, const uint32_t* B_old,
     if (n == 0) return cudaSuccess;
     k_bucket_layout<<<grid_for(n, 256), 256, 0, s>>>(perm, B_old, s_old, tr_old, n, bstart, brec, biv,
                                                       B_new, s_new, tr_new, rb, stride, ib);
+    LAUNCH_DONE();
+}
+
+cudaError_t launch_iota_u64(unsigned long long* out, long long n, unsigned long long base, cudaStream_t s,
+                            unsigned long long* launches) {
+    if (n == 0) return cudaSuccess;
+    k_iota_u64<<<grid_for(n, 256), 256, 0, s>>>(out, n, base);
+    LAUNCH_DONE();
+}
+
+cudaError_t launch_count_nonzero_u8(const uint8_t* x, long long n, unsigned long long* count, cudaStream_t s,
+                                    unsigned long long* launches) {
+    if (n == 0) return cudaSuccess;
+    k_count_nonzero_u8<<<grid_for(n, 256), 256, 0, s>>>(x, n, count);
     LAUNCH_DONE();
 }
 

@@ -153,6 +153,11 @@ cudaError_t launch_bucket_layout(const uint32_t* perm, const uint32_t* B_old,
                                  unsigned long long* rec_base, uint32_t* stride,
                                  unsigned long long* iv_base, cudaStream_t s,
                                  unsigned long long* launches);
+cudaError_t launch_iota_u64(unsigned long long* out, long long n, unsigned long long base, cudaStream_t s,
+                            unsigned long long* launches);
+// count += number of nonzero bytes in x[0, n)
+cudaError_t launch_count_nonzero_u8(const uint8_t* x, long long n, unsigned long long* count, cudaStream_t s,
+                                    unsigned long long* launches);
 cudaError_t launch_gather_field(const StoreView& old_st, const uint32_t* perm, long long n,
                                 const unsigned long long* rec_base_new, const uint32_t* stride_new,
                                 const void* src, void* dst, int elem_bytes, cudaStream_t s,
