@@ -163,7 +163,10 @@ int prc_gpu_ctx_rank(const prc_gpu_ctx* ctx, int* rank, int* world);
  * Morton distance between the packets of one warp (default 64); "per_species" 1 = the
  * device-resident iteration (prc_gpu_opt_step) computes per-type gradients of every
  * species (config (c)); the optimiser still updates the unknown species; "pad" 0 turns
- * off the guard-free walks over the padded voxel layout (default 1; same results). */
+ * off the guard-free walks over the padded voxel layout (default 1; same results);
+ * "grad_copies" = most copies of the padded gradient the gradient kernel reduces into
+ * (0 = default 4, fewer when they would exceed 80 MB; applied at the next scene upload;
+ * same results up to the order of floating-point sums). */
 int prc_gpu_ctx_set_option(prc_gpu_ctx* ctx, const char* key, int64_t value);
 
 /* Uploads (and validates, finalizes) the scene; replaces any previous scene and
