@@ -142,6 +142,9 @@ struct prc_gpu_ctx {
     // forward-reuse cache: grad_forward right after recycled_render at the same point
     // (inverse.cpp:205, 246) reuses the stored forward instead of recomputing K3/K4
     unsigned long long fwd_gen = 0;
+    // bumped whenever cameras, scene or options change: invalidates every store's cached
+    // event geometry (prc_gpu_store::geo_key)
+    unsigned long long geo_gen = 1;
     unsigned long long last_fwd_gen = ~0ull, last_fwd_key = 0;
     const prc_gpu_store* last_fwd_store = nullptr;
     unsigned long long last_fwd_clamps = 0;
@@ -188,6 +191,8 @@ struct prc_gpu_store {
     unsigned long long n_rec = 0, n_iv = 0;
     DBuf<float> ev_val;    // event cache: [det][iv] (path mode) or [det][vt] (wavefront)
     DBuf<int32_t> ev_pix;
+    DBuf<int32_t> ev_c1;   // wavefront: beta-independent event term (VertexTable::ev_c1)
+    unsigned long long geo_key = 0;  // == ctx geo_gen while ev_pix / ev_c1 hold the geometry
     DBuf<double> lp, own;  // per interaction vertex: log-prefix (K4a), weight sum (K5b)
     bool vt_ready = false; // Morton-ordered vertex table (wavefront mapping)
     DBuf<double> vt_x, vt_y, vt_z, vt_dx, vt_dy, vt_dz;
@@ -240,7 +245,7 @@ struct prc_gpu_store {
     unsigned long long device_bytes() const {
         return B.bytes() + stride.bytes() + stream.bytes() + rec_base.bytes() + iv_base.bytes() +
                trunc.bytes() + px.bytes() * 8 + vox.bytes() + meta.bytes() + ev_val.bytes() +
-               ev_pix.bytes() + br_tot64.bytes() + sp_ref.bytes() + br_tot.bytes() + lp.bytes() +
+               ev_pix.bytes() + ev_c1.bytes() + br_tot64.bytes() + sp_ref.bytes() + br_tot.bytes() + lp.bytes() +
                own.bytes() + vt_x.bytes() * 6 + vt_vox.bytes() + vt_meta.bytes() + vt_iv.bytes();
     }
 };
@@ -297,6 +302,7 @@ long long finalize_detectors(DScene& s, const prc_detector_desc* dd, int n, cons
 }
 
 void upload_scene(prc_gpu_ctx* c, const prc_scene_desc* d) {
+    ++c->geo_gen;  // cameras / species / surfaces may change: cached event geometry is stale
     if (d->n_species < 0 || d->n_species > PRC_MAX_SPECIES)
         throw Err(PRC_ERR_CONFIG, "scene: species count outside 0..16");
     if (d->n_surfaces < 0 || d->n_surfaces > PRC_MAX_SURF)
@@ -387,6 +393,29 @@ void upload_scene(prc_gpu_ctx* c, const prc_scene_desc* d) {
     s.n_det = d->n_detectors;
     const long long off = finalize_detectors(s, d->detectors, d->n_detectors, nullptr, nullptr);
     s.n_pix = off;
+    // Fixed-point event term of single-species scenes (DScene::c1_fast): the range of
+    // log(albedo * f) over cos in [-1, 1], from the phase function's extremes.
+    s.c1_fast = 0;
+    if (s.n_species == 1 && s.sp[0].albedo > 0.0) {
+        const DSpecies& sp = s.sp[0];
+        double fmin, fmax;
+        if (sp.kind == 1) {
+            fmin = 3.0 / (16.0 * PRC_PI);
+            fmax = 6.0 / (16.0 * PRC_PI);
+        } else {
+            const double g = std::fabs(sp.g);
+            fmin = (1.0 - g * g) / (4.0 * PRC_PI * std::pow(1.0 + g, 3.0));
+            fmax = (1.0 - g * g) / (4.0 * PRC_PI * std::pow(1.0 - g, 3.0));
+        }
+        const double lo = std::log(sp.albedo * fmin), hi = std::log(sp.albedo * fmax);
+        const double h = 0.5 * (hi - lo) + 1.0;  // + margin for cos_le rounding past +-1
+        if (std::isfinite(lo) && std::isfinite(hi) && h < 64.0) {
+            s.c1_fast = 1;
+            s.c1_mid = 0.5 * (lo + hi);
+            s.c1_q = std::ldexp(1.0, (int)std::floor(std::log2(1073741824.0 / h)));
+            s.c1_iq = 1.0 / s.c1_q;
+        }
+    }
     // Guard-free walks over the padded layout (prc_device.cuh, dda_walk_pad): exact when
     // the rounding of the tmax sums (~512 ulp of a distance <= 4R) stays far below a voxel.
     if (s.has_medium) {
@@ -540,6 +569,7 @@ struct EvalRun {
 // their position (built once per store layout; geometry only, so valid for any beta).
 void ensure_vertex_table(prc_gpu_ctx* c, prc_gpu_store* st) {
     if (st->vt_ready) return;
+    st->geo_key = 0;  // the event cache indexes the vertex table
     const long long n = (long long)st->n_iv;
     cudaStream_t q = c->stream;
     const size_t nn = (size_t)std::max<long long>(n, 1);
@@ -584,6 +614,8 @@ VertexTable vertex_table(prc_gpu_store* st) {
     v.iv = st->vt_iv.p;
     v.ev_val = st->ev_val.p;
     v.ev_pix = st->ev_pix.p;
+    v.ev_c1 = st->ev_c1.p;
+    v.geo_ready = st->geo_key == st->ctx->geo_gen ? 1 : 0;
     return v;
 }
 
@@ -630,8 +662,10 @@ void run_forward(prc_gpu_ctx* c, prc_gpu_store* st, const Resolved& r, const Eva
         phong_dev = c->phong.p;
     }
     const size_t slots = (size_t)s.n_det * (size_t)std::max<unsigned long long>(st->n_iv, 1);
+    if (st->ev_val.n < slots || st->ev_pix.n < slots || (c->mode == 0 && st->ev_c1.n < slots)) st->geo_key = 0;
     st->ev_val.grow(slots);
     st->ev_pix.grow(slots);
+    if (c->mode == 0) st->ev_c1.grow(slots);
     st->lp.grow((size_t)std::max<unsigned long long>(st->n_iv, 1));
     st->own.grow((size_t)std::max<unsigned long long>(st->n_iv, 1));
     ++c->fwd_gen;  // invalidates any cached forward
@@ -646,7 +680,9 @@ void run_forward(prc_gpu_ctx* c, prc_gpu_store* st, const Resolved& r, const Eva
         CK(launch_prefix(s, st->view(), ea, st->lp.p, q, &c->launches));
         CK(cudaEventRecord(c->ev[6], q));
         CK(launch_le_forward(s, vertex_table(st), ea, st->lp.p, q, &c->launches));
+        st->geo_key = c->geo_gen;  // K4b wrote the event geometry (stream-ordered for later launches)
     } else {
+        st->geo_key = 0;  // the per-path kernels reuse ev_pix in path layout
         CK(launch_forward(s, st->view(), ea, q, &c->launches));
     }
     CK(cudaEventRecord(c->ev[2], q));
@@ -1357,6 +1393,7 @@ PRC_EXPORT int prc_gpu_ctx_set_option(prc_gpu_ctx* ctx, const char* key, int64_t
         return fail(PRC_ERR_CONFIG, "unknown option " + k);
     }
     ++ctx->fwd_gen;  // a cached forward was computed under the old options
+    ++ctx->geo_gen;
     return PRC_OK;
 }
 
@@ -1831,6 +1868,7 @@ static void set_resolution(prc_gpu_ctx* c, const std::vector<int>& rows, const s
     c->images.alloc((size_t)n_pix);
     c->weights.alloc((size_t)n_pix);
     c->opt_gt.alloc((size_t)n_pix);
+    ++c->geo_gen;  // pixel_of changes with the resolution
     ++c->fwd_gen;
 }
 

@@ -12,6 +12,16 @@ __device__ __forceinline__ double scat_num(const DScene& sc, const float* sp, in
         num += sc.sp[j].albedo * (double)sp[(long long)j * sc.V + vox] * phase_eval(sc.sp[j], c);
     return num;
 }
+// Fixed-point event term of single-species scenes (DScene::c1_fast): c1 = log(albedo * f)
+// -> q with c1 ~ c1_mid + q * c1_iq; INT32_MIN when albedo * f == 0 (no event).
+__device__ __forceinline__ int32_t c1_quant(const DScene& sc, double c1) {
+    if (!(c1 > -INFINITY)) return INT32_MIN;
+    const double q = rint((c1 - sc.c1_mid) * sc.c1_q);
+    return (int32_t)fmin(fmax(q, -2147483000.0), 2147483000.0);
+}
+__device__ __forceinline__ double c1_dequant(const DScene& sc, int32_t q) {
+    return sc.c1_mid + (double)q * sc.c1_iq;
+}
 __device__ __forceinline__ double ext_num(const DScene& sc, const float* sp, int vox, double c) {
     double num = 0.0;  // ext_num_ref, pathstore.cpp:90-94
     for (int j = 0; j < sc.n_species; ++j)

@@ -37,8 +37,15 @@ struct VertexTable {
     const int32_t* vox;
     const uint32_t* meta;
     const uint32_t* iv;  // interaction-vertex slot (path-layout index) of entry i
-    float* ev_val;       // [det][i] cached event value (K4b -> K5b)
-    int32_t* ev_pix;     // [det][i] pixel, -1 when no event
+    float* ev_val;       // [det][i] cached event value (K4b -> K5b), 0 when no event
+    int32_t* ev_pix;     // [det][i] pixel, -1 when no event (geometric: dead vertices keep theirs)
+    // Beta-independent part of a single-species volume event's value (K4b): c1 =
+    // log(albedo * phase(cos_le)) in fixed point (DScene::c1_fast; INT32_MIN = no event).
+    // Written with ev_pix by the first forward over a store, read by later ones
+    // (geo_ready), which then skip pixel_of, the visibility tests, the phase function and
+    // its log.
+    int32_t* ev_c1;      // [det][i]
+    int geo_ready;
 };
 
 struct RecordsOut {

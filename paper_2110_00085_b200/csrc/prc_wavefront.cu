@@ -191,49 +191,84 @@ __global__ void __launch_bounds__(kWF, kFwdMinBlocks) k_le_forward(const __grid_
     // lp - log(den) is per vertex: one log per camera event instead of two (the sum is
     // re-associated, a change of ~1e-16 relative in the event value)
     const double lbase = den > 0.0 ? lpv - log(den) : 0.0;
+    // Single-species volume events (DScene::c1_fast): log value = [lp - log(den) +
+    // log(beta_t[vox])] + c1 with c1 = log(albedo * f(cos_le)) in fixed point.  The bracket is
+    // per vertex; c1 and the pixel do not depend on beta, so after the first forward over
+    // a store they come from the cache (geo_ready) and the event needs only its walk.  Both
+    // paths evaluate the same expression, so a recycled image at the sampling point still
+    // equals the fresh render.
+    const bool c1v = sc.c1_fast && kind == VK_VOLUME;
+    const bool fast = c1v && vt.geo_ready && sc.pad_walk;
+    double lvol = -INFINITY;
+    if (c1v && live && den > 0.0) {
+        const double bt = (double)ea.sp_t[vox];
+        if (bt > 0.0) lvol = lbase + log(bt);
+    }
     unsigned clamps = 0;
     for (int k = 0; k < sc.n_det; ++k) {
-        float val = 0.0f;
+        const unsigned long long e = (unsigned long long)k * vt.n + i;
+        // vertex position re-read per camera (L1 hits) instead of being kept live across
+        // the DDA: frees registers for the walk's loop invariants
+        const V3 x = mk(vt.x[i], vt.y[i], vt.z[i]);
         int pix = -1;
-        double contrib = 0.0;
-        if (live) {
-            // vertex position/direction re-read per camera (L1 hits) instead of being kept
-            // live across the DDA: frees registers for the walk's loop invariants
-            const V3 x = mk(vt.x[i], vt.y[i], vt.z[i]);
+        int32_t q = INT32_MIN;
+        V3 w;
+        double r = 0.0, geom = 0.0, logval = -INFINITY;
+        if (fast) {
+            if (lvol != -INFINITY) {
+                pix = vt.ev_pix[e];
+                q = vt.ev_c1[e];
+                if (pix >= 0 && q != INT32_MIN) {
+                    // w, r and geom exactly as event_geometry (the walk's indexing is bit-exact)
+                    const V3 to_det = ld3(sc.det[k].pos) - x;
+                    r = norm3(to_det);
+                    w = to_det * (1.0 / r);
+                    geom = 1.0 / (r * r);
+                    logval = lvol + c1_dequant(sc, q);
+                }
+            }
+        } else if (act && (live || !vt.geo_ready)) {
             const DDet& D = sc.det[k];
             pix = pixel_of(D, x);
-            V3 w;
-            double r, geom, cos_le;
+            double cos_le;
             if (pix >= 0 &&
                 event_geometry(sc, D, x, mk(vt.dx[i], vt.dy[i], vt.dz[i]), kind, surf, w, r, geom, cos_le)) {
-                double logval = -INFINITY;
-                if (kind == VK_VOLUME) {
-                    const double num = scat_num(sc, ea.sp_t, vox, cos_le);
-                    if (num > 0.0 && den > 0.0) logval = lbase + log(num);
-                } else {
+                if (c1v) {
+                    q = c1_quant(sc, log(sc.sp[0].albedo * phase_eval(sc.sp[0], cos_le)));
+                    if (lvol != -INFINITY && q != INT32_MIN) logval = lvol + c1_dequant(sc, q);
+                } else if (kind == VK_VOLUME) {
+                    if (live) {
+                        const double num = scat_num(sc, ea.sp_t, vox, cos_le);
+                        if (num > 0.0 && den > 0.0) logval = lbase + log(num);
+                    }
+                } else if (live) {
                     const double fr = surf_brdf(sc, ea.phong, surf, cos_le);
                     if (fr > 0.0) logval = lpv + log(fr);
-                }
-                if (logval != -INFINITY) {
-                    if (sc.has_medium) {
-                        logval -= sc.pad_walk ? dda_optical_depth_pad(sc, x, w, r, ea.bt_pad)
-                                              : dda_optical_depth(sc, x, w, r, ea.bt_tot);
-                    }
-                    if (logval > PRC_LOG_CLAMP || logval < -PRC_LOG_CLAMP) {
-                        logval = clampd(logval, -PRC_LOG_CLAMP, PRC_LOG_CLAMP);
-                        ++clamps;
-                    }
-                    contrib = exp(logval) * geom * sc.prefactor;
-                    val = (float)contrib;
                 }
             } else {
                 pix = -1;
             }
         }
-        if (contrib != 0.0) atomicAdd(ea.images + sc.det[k].img_off + pix, contrib);
+        float val = 0.0f;
+        if (logval != -INFINITY) {
+            if (sc.has_medium) {
+                logval -= sc.pad_walk ? dda_optical_depth_pad(sc, x, w, r, ea.bt_pad)
+                                      : dda_optical_depth(sc, x, w, r, ea.bt_tot);
+            }
+            if (logval > PRC_LOG_CLAMP || logval < -PRC_LOG_CLAMP) {
+                logval = clampd(logval, -PRC_LOG_CLAMP, PRC_LOG_CLAMP);
+                ++clamps;
+            }
+            const double contrib = exp(logval) * geom * sc.prefactor;
+            val = (float)contrib;
+            if (contrib != 0.0) atomicAdd(ea.images + sc.det[k].img_off + pix, contrib);
+        }
         if (act) {
-            vt.ev_val[(unsigned long long)k * vt.n + i] = val;
-            vt.ev_pix[(unsigned long long)k * vt.n + i] = pix;
+            vt.ev_val[e] = val;
+            if (!vt.geo_ready) {  // the event geometry, cached for later forwards over this store
+                vt.ev_pix[e] = pix;
+                vt.ev_c1[e] = q;
+            }
         }
     }
     for (int o = 16; o > 0; o >>= 1) clamps += __shfl_down_sync(0xffffffffu, clamps, o);
