@@ -477,6 +477,13 @@ __global__ void __launch_bounds__(128, M == 2 ? PRC_GRAD2_MINB : (M == 3 ? PRC_G
                 cf[r] = -w;
                 if (kind == VK_VOLUME) {
                     const int vox = vt.vox[i];
+                    if (single && sc.c1_fast && !ea.legacy) {
+                        // one species: albedo f / (albedo beta_t f) = 1 / beta_t (score_term,
+                        // pathstore.cpp:97-105), no phase-function evaluations per event
+                        const double bt = (double)ea.sp_t[vox];
+                        if (bt > 0.0) acc[r] += w / bt;
+                        continue;
+                    }
                     const double num = ea.legacy ? 0.0 : scat_num(sc, ea.sp_t, vox, cos_le);
                     if (single) {
                         acc[r] += w * score_j(sc, ea, sc.unknown, vox, cos_le, num);
