@@ -236,7 +236,7 @@ def run_ours(args):
     bytes_pass = 8.0 * W_live + 64.0 * vert_global + 16.0 * E
     bytes_iter = 2.0 * bytes_pass
     peak, peak_kind = measured_peak()
-    # Dominant kernel (launch list: profiles/r11_kernels_1e8.md): K5b, the LE-ray gradient
+    # Dominant kernel (launch list: profiles/r12_kernels_1e8.md): K5b, the LE-ray gradient
     # scatter.  Its event-timed duration is the gradient phase minus K5a (+ the padded
     # fold), and its algorithmic bytes are the §8(d) per-unit figures over the units it
     # processes: 8 B per LE span incidence, 16 B per event, 64 B per vertex.
