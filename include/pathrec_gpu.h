@@ -222,6 +222,9 @@ int prc_gpu_store_sizes(const prc_gpu_store* store, uint32_t* out);
 int prc_gpu_store_export_pstr(prc_gpu_ctx* ctx, const prc_gpu_store* store, const char* path);
 int prc_gpu_store_import_pstr(prc_gpu_ctx* ctx, const char* path, prc_gpu_store** out);
 int prc_gpu_store_set_generation(prc_gpu_store* store, uint64_t generation);
+/* A store belongs to the context that made it: passing it with another context returns
+ * PRC_ERR_INVALID.  prc_gpu_store_free is valid before or after that context is destroyed
+ * (a store outliving its context can only be freed). */
 void prc_gpu_store_free(prc_gpu_store* store);
 
 /* ---------------------------------------------------------------------------

@@ -10,6 +10,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <set>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -152,6 +153,7 @@ struct prc_gpu_ctx {
     cudaEvent_t ev[9] = {};  // [0..5] phases, [6] after K4a, [7] before K5a, [8] spare
     cudaEvent_t timer[2] = {};
     double last_ms[8] = {};
+    std::set<prc_gpu_store*> stores;  // live stores made by this context (orphaned on destroy)
     int g_pad_copies = 1;  // see EvalArgs::g_pad_copies
     int grad_copies_max = 0;  // option "grad_copies" (applied at scene upload); 0: 4
     ~prc_gpu_ctx() {
@@ -178,7 +180,8 @@ struct prc_gpu_ctx {
 };
 
 struct prc_gpu_store {
-    prc_gpu_ctx* ctx = nullptr;
+    prc_gpu_ctx* ctx = nullptr;  // null once the context is destroyed (the store stays freeable)
+    int device = 0;
     unsigned long long n = 0, n_global = 0, stream_base = 0, seed = 0, generation = 0;
     bool sorted = false;
     int max_B = 0;
@@ -203,6 +206,14 @@ struct prc_gpu_store {
     std::vector<double> ref_beta;
     double ref_kappa = 0.0, ref_gamma = 0.0;
     unsigned long long segments = 0, truncated = 0;
+
+    prc_gpu_store() = default;
+    explicit prc_gpu_store(prc_gpu_ctx* c) : ctx(c), device(c->device) { c->stores.insert(this); }
+    prc_gpu_store(const prc_gpu_store&) = delete;
+    prc_gpu_store& operator=(const prc_gpu_store&) = delete;
+    ~prc_gpu_store() {
+        if (ctx) ctx->stores.erase(this);
+    }
 
     StoreView view() {
         StoreView v{};
@@ -303,6 +314,7 @@ long long finalize_detectors(DScene& s, const prc_detector_desc* dd, int n, cons
 
 void upload_scene(prc_gpu_ctx* c, const prc_scene_desc* d) {
     ++c->geo_gen;  // cameras / species / surfaces may change: cached event geometry is stale
+    ++c->fwd_gen;  // and so is a cached forward (grad_forward after recycled_render)
     if (d->n_species < 0 || d->n_species > PRC_MAX_SPECIES)
         throw Err(PRC_ERR_CONFIG, "scene: species count outside 0..16");
     if (d->n_surfaces < 0 || d->n_surfaces > PRC_MAX_SURF)
@@ -762,8 +774,7 @@ std::unique_ptr<prc_gpu_store> trace_store(prc_gpu_ctx* c, const prc_gpu_render_
                                            const double* ref_beta_host_or_dev, bool ref_on_dev) {
     const DScene& s = c->dsc;
     cudaStream_t q = c->stream;
-    auto st = std::make_unique<prc_gpu_store>();
-    st->ctx = c;
+    auto st = std::make_unique<prc_gpu_store>(c);
     const unsigned long long N = o->n_paths;
     st->n_global = N;
     st->stream_base = N * (unsigned long long)c->rank / (unsigned long long)c->world;
@@ -1166,8 +1177,7 @@ std::unique_ptr<prc_gpu_store> import_pstr(prc_gpu_ctx* c, const std::string& pa
     if (!is || std::memcmp(magic, "PSTR", 4) != 0)
         throw Err(PRC_ERR_IO, "load_store: bad magic at offset 0 in " + path);
     if (get<uint32_t>(is) != 1) throw Err(PRC_ERR_IO, "load_store: unsupported version");
-    auto st = std::make_unique<prc_gpu_store>();
-    st->ctx = c;
+    auto st = std::make_unique<prc_gpu_store>(c);
     const uint64_t count = get<uint64_t>(is);
     st->generation = get<uint64_t>(is);
     st->seed = get<uint64_t>(is);
@@ -1368,6 +1378,7 @@ PRC_EXPORT int prc_gpu_ctx_create_rank(int device, int rank, int world, const vo
 PRC_EXPORT void prc_gpu_ctx_destroy(prc_gpu_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
+    for (prc_gpu_store* st : ctx->stores) st->ctx = nullptr;  // still freeable by the caller
     delete ctx;
 }
 
@@ -1475,6 +1486,7 @@ PRC_EXPORT int prc_gpu_render(prc_gpu_ctx* ctx, const prc_gpu_render_opts* opts,
 
 PRC_EXPORT int prc_gpu_sort_by_size(prc_gpu_ctx* ctx, prc_gpu_store* store) {
     if (!ctx || !store) return fail(PRC_ERR_INVALID, "prc_gpu_sort_by_size: null argument");
+    if (store->ctx != ctx) return fail(PRC_ERR_INVALID, "prc_gpu_sort_by_size: the store belongs to another context");
     ABI_TRY
     begin(ctx);
     sort_store(ctx, store);
@@ -1500,6 +1512,7 @@ PRC_EXPORT int prc_gpu_store_info_get(const prc_gpu_store* st, prc_gpu_store_inf
 
 PRC_EXPORT int prc_gpu_store_streams(const prc_gpu_store* st, uint64_t* out) {
     if (!st || !out) return fail(PRC_ERR_INVALID, "prc_gpu_store_streams: null argument");
+    if (!st->ctx) return fail(PRC_ERR_INVALID, "prc_gpu_store_streams: the store's context was destroyed");
     ABI_TRY
     begin(st->ctx);
     if (st->n) CK(cudaMemcpy(out, st->stream.p, st->n * 8, cudaMemcpyDeviceToHost));
@@ -1508,6 +1521,7 @@ PRC_EXPORT int prc_gpu_store_streams(const prc_gpu_store* st, uint64_t* out) {
 
 PRC_EXPORT int prc_gpu_store_sizes(const prc_gpu_store* st, uint32_t* out) {
     if (!st || !out) return fail(PRC_ERR_INVALID, "prc_gpu_store_sizes: null argument");
+    if (!st->ctx) return fail(PRC_ERR_INVALID, "prc_gpu_store_sizes: the store's context was destroyed");
     ABI_TRY
     begin(st->ctx);
     if (st->n) CK(cudaMemcpy(out, st->B.p, st->n * 4, cudaMemcpyDeviceToHost));
@@ -1517,6 +1531,7 @@ PRC_EXPORT int prc_gpu_store_sizes(const prc_gpu_store* st, uint32_t* out) {
 PRC_EXPORT int prc_gpu_store_export_pstr(prc_gpu_ctx* ctx, const prc_gpu_store* store,
                                          const char* path) {
     if (!ctx || !store || !path) return fail(PRC_ERR_INVALID, "prc_gpu_store_export_pstr: null argument");
+    if (store->ctx != ctx) return fail(PRC_ERR_INVALID, "prc_gpu_store_export_pstr: the store belongs to another context");
     ABI_TRY
     begin(ctx);
     export_pstr(ctx, const_cast<prc_gpu_store*>(store), path);
@@ -1541,8 +1556,8 @@ PRC_EXPORT int prc_gpu_store_set_generation(prc_gpu_store* st, uint64_t g) {
 
 PRC_EXPORT void prc_gpu_store_free(prc_gpu_store* st) {
     if (!st) return;
-    cudaSetDevice(st->ctx->device);
-    ++st->ctx->fwd_gen;  // a later store may reuse this address
+    cudaSetDevice(st->device);
+    if (st->ctx) ++st->ctx->fwd_gen;  // a later store may reuse this address
     delete st;
 }
 
@@ -1553,6 +1568,7 @@ PRC_EXPORT int prc_gpu_evaluate(prc_gpu_ctx* ctx, const prc_gpu_store* store,
     const int flags = opts ? opts->flags : PRC_EVAL_NORMALIZE;
     if (flags & PRC_EVAL_SELF_NORMALIZE)
         return fail(PRC_ERR_CONFIG, "self_normalize is not supported by the recycling engine");
+    if (store->ctx != ctx) return fail(PRC_ERR_INVALID, "prc_gpu_evaluate: the store belongs to another context");
     ABI_TRY
     begin(ctx);
     ctx->check_scene();
@@ -1725,6 +1741,7 @@ PRC_EXPORT int prc_gpu_opt_init(prc_gpu_ctx* ctx, const prc_gpu_params* initial,
 PRC_EXPORT int prc_gpu_opt_step(prc_gpu_ctx* ctx, const prc_gpu_store* store, double* loss_out) {
     if (!ctx || !store) return fail(PRC_ERR_INVALID, "prc_gpu_opt_step: null argument");
     if (!ctx->opt_ready) return fail(PRC_ERR_INVALID, "prc_gpu_opt_step: optimizer not initialised");
+    if (store->ctx != ctx) return fail(PRC_ERR_INVALID, "prc_gpu_opt_step: the store belongs to another context");
     ABI_TRY
     begin(ctx);
     const double l = opt_step(ctx, const_cast<prc_gpu_store*>(store));
@@ -2142,6 +2159,7 @@ PRC_EXPORT int prc_gpu_timer_stop(prc_gpu_ctx* ctx, double* ms) {
 
 PRC_EXPORT int prc_gpu_store_stats(prc_gpu_ctx* ctx, const prc_gpu_store* store, uint64_t* out4) {
     if (!ctx || !store || !out4) return fail(PRC_ERR_INVALID, "null argument");
+    if (store->ctx != ctx) return fail(PRC_ERR_INVALID, "prc_gpu_store_stats: the store belongs to another context");
     ABI_TRY
     begin(ctx);
     ctx->check_scene();

@@ -103,6 +103,11 @@ __device__ __forceinline__ void vertex_scores(const DScene& sc, const EvalArgs& 
         for (int j = 0; j < n_out; ++j) atomicAdd(ea.g_vert + (long long)j * sc.V + vox, wgt * s);
         return;
     }
+    if (sc.c1_fast && !ea.per_species) {  // one species: albedo f / (albedo beta_t f) = 1 / beta_t
+        const double bt = (double)ea.sp_t[vox];
+        if (bt > 0.0) atomicAdd(ea.g_vert + vox, wgt / bt);
+        return;
+    }
     const double num = scat_num(sc, ea.sp_t, vox, c);
     if (!(num > 0.0)) return;
     if (ea.per_species) {

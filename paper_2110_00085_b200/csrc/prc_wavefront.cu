@@ -152,12 +152,21 @@ __global__ void __launch_bounds__(kTPB) k_prefix(const __grid_constant__ DScene 
         const double ct = st.ct[r];
         if (kind == VK_VOLUME) {  // continuation, pathstore.cpp:168-184
             const int vox = st.vox[r];
-            const double num = scat_num(sc, ea.sp_t, vox, ct);
-            const double den = ext_num(sc, ea.sp_ref, vox, ct);
-            if (num <= 0.0 || den <= 0.0)
-                dead = true;
-            else
-                l += log(num) - log(den);
+            if (sc.c1_fast) {  // one species: the phase function cancels
+                const double num = sc.sp[0].albedo * (double)ea.sp_t[vox];
+                const double den = (double)ea.sp_ref[vox];
+                if (num <= 0.0 || den <= 0.0)
+                    dead = true;
+                else
+                    l += log(num) - log(den);
+            } else {
+                const double num = scat_num(sc, ea.sp_t, vox, ct);
+                const double den = ext_num(sc, ea.sp_ref, vox, ct);
+                if (num <= 0.0 || den <= 0.0)
+                    dead = true;
+                else
+                    l += log(num) - log(den);
+            }
         } else if (kind == VK_SURFACE) {
             const double fr = surf_brdf(sc, ea.phong, meta_surface(m), ct);
             if (fr <= 0.0)

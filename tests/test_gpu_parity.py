@@ -589,3 +589,70 @@ def test_opt_step_per_type_mode_matches_single_unknown(ctx, golden_dir):
         out.append(ctx.opt_params().beta)
     ctx.set_option("per_species", 0)
     assert np.abs(out[0] - out[1]).max() <= 1e-9 + 1e-6 * 0.05
+
+
+def test_event_geometry_cache_follows_the_cameras(ctx, golden_dir):
+    """K4b caches each event's pixel and log(albedo f) per store (single-species scenes).
+    A new camera set (scene upload) must invalidate it: evaluating a store after switching
+    cameras equals evaluating it in a context that only ever saw the new cameras."""
+    from paper_2110_00085_b200.gpu import Context
+    a = S.cloud_scene(12, 10, 10)
+    b = S.cloud_scene(12, 7, 9, n_ring=5, fov=0.7)
+    ctx.upload(a)
+    st = ctx.load_store(str(golden_dir / "cloud.pstr"))
+    t = perturbed(a)
+    for _ in range(2):  # build the cache, then use it
+        ctx.evaluate_store(a, st, t, EvalOptions())
+    ctx.upload(b)
+    w = np.linspace(-1.0, 1.0, b.pixel_count)
+    got = [ctx.evaluate_store(b, st, t, EvalOptions(want_grad=True, pixel_weights=w)) for _ in range(2)]
+    fresh = Context(0)
+    try:
+        fresh.upload(b)
+        st2 = fresh.load_store(str(golden_dir / "cloud.pstr"))
+        ref = fresh.evaluate_store(b, st2, t, EvalOptions(want_grad=True, pixel_weights=w))
+    finally:
+        fresh.close()
+    for r in got:
+        assert img_err(r.images, ref.images) <= 1e-12
+        assert grad_err(r.grad_beta, ref.grad_beta) <= 1e-12
+
+
+def test_gradient_copies_option_same_results(ctx, golden_dir):
+    """K5b's reductions into 1 or 4 copies of the padded gradient give the same gradient
+    up to the order of floating-point sums."""
+    scene = FIXTURES["cloud"]["scene"]()
+    w = weight_patterns(scene)["res"]
+    out = []
+    for copies in (1, 4):
+        ctx.set_option("grad_copies", copies)
+        ctx.upload(scene)
+        st = ctx.load_store(str(golden_dir / "cloud.pstr"))
+        out.append(ctx.evaluate_store(scene, st, perturbed(scene), EvalOptions(want_grad=True, pixel_weights=w)))
+    ctx.set_option("grad_copies", 0)
+    ctx.upload(scene)
+    assert img_err(out[1].images, out[0].images) <= 1e-12
+    assert grad_err(out[1].grad_beta, out[0].grad_beta) <= 1e-12
+
+
+def test_store_outlives_its_context(golden_dir):
+    """Stores belong to their context (another context gets PRC_ERR_INVALID) and can be
+    freed after the context is destroyed (the C ABI orphans them instead of dangling)."""
+    from paper_2110_00085_b200.gpu import Context, PrcInvalidError
+    scene = FIXTURES["cloud"]["scene"]()
+    a, b = Context(0), Context(0)
+    try:
+        a.upload(scene)
+        b.upload(scene)
+        st = a.load_store(str(golden_dir / "cloud.pstr"))
+        with pytest.raises(PrcInvalidError):
+            b.evaluate_store(scene, st, None, EvalOptions())
+        a.close()
+        with pytest.raises(PrcInvalidError):
+            st.sizes()
+        st.free()  # no use-after-free of the destroyed context
+        st2 = b.load_store(str(golden_dir / "cloud.pstr"))
+        assert b.evaluate_store(scene, st2, None, EvalOptions()).images.sum() > 0
+    finally:
+        a.close()
+        b.close()
