@@ -38,7 +38,7 @@ CONFIGS = {
               desc="2-species 128^3 cloud (HG 0.85 + Rayleigh), 9 cameras 128x128, 1e8 paths, per-type gradients"),
     "d": dict(n=0, rows=256, two=False, paths=10_000_000,
               desc="reflectometry: Phong sphere + 14 diffuse spheres in a Phong box, 16 views 256x256, 1e7 paths"),
-    # (e): 1e9 paths over the job, at most 1.25e8 per GPU (the store is ~1 KB/path, so
+    # (e): 1e9 paths over the job, at most 1.25e8 per GPU (the store is ~1.2 KB/path, so
     # 1e9 needs 8 GPUs of 180 GB); recycled iterations timed as in (b), resampling every
     # N_r = 30 iterations reported amortised
     "e": dict(n=256, rows=128, two=False, paths=1_000_000_000, per_gpu_cap=125_000_000,
