@@ -195,6 +195,7 @@ struct prc_gpu_store {
     DBuf<float> ev_val;    // event cache: [det][iv] (path mode) or [det][vt] (wavefront)
     DBuf<int32_t> ev_pix;
     DBuf<int32_t> ev_c1;   // wavefront: beta-independent event term (VertexTable::ev_c1)
+    DBuf<float> ev_f;      // wavefront, 2..4 species: phase values (VertexTable::ev_f)
     unsigned long long geo_key = 0;  // == ctx geo_gen while ev_pix / ev_c1 hold the geometry
     DBuf<double> lp, own;  // per interaction vertex: log-prefix (K4a), weight sum (K5b)
     bool vt_ready = false; // Morton-ordered vertex table (wavefront mapping)
@@ -256,7 +257,7 @@ struct prc_gpu_store {
     unsigned long long device_bytes() const {
         return B.bytes() + stride.bytes() + stream.bytes() + rec_base.bytes() + iv_base.bytes() +
                trunc.bytes() + px.bytes() * 8 + vox.bytes() + meta.bytes() + ev_val.bytes() +
-               ev_pix.bytes() + ev_c1.bytes() + br_tot64.bytes() + sp_ref.bytes() + br_tot.bytes() + lp.bytes() +
+               ev_pix.bytes() + ev_c1.bytes() + ev_f.bytes() + br_tot64.bytes() + sp_ref.bytes() + br_tot.bytes() + lp.bytes() +
                own.bytes() + vt_x.bytes() * 6 + vt_vox.bytes() + vt_meta.bytes() + vt_iv.bytes();
     }
 };
@@ -428,6 +429,7 @@ void upload_scene(prc_gpu_ctx* c, const prc_scene_desc* d) {
             s.c1_iq = 1.0 / s.c1_q;
         }
     }
+    s.fcache = s.n_species >= 2 && s.n_species <= kFCacheMax ? 1 : 0;
     // Guard-free walks over the padded layout (prc_device.cuh, dda_walk_pad): exact when
     // the rounding of the tmax sums (~512 ulp of a distance <= 4R) stays far below a voxel.
     if (s.has_medium) {
@@ -629,6 +631,7 @@ VertexTable vertex_table(prc_gpu_store* st) {
     v.ev_val = st->ev_val.p;
     v.ev_pix = st->ev_pix.p;
     v.ev_c1 = st->ev_c1.p;
+    v.ev_f = st->ev_f.p;
     v.geo_ready = st->geo_key == st->ctx->geo_gen ? 1 : 0;
     return v;
 }
@@ -676,10 +679,16 @@ void run_forward(prc_gpu_ctx* c, prc_gpu_store* st, const Resolved& r, const Eva
         phong_dev = c->phong.p;
     }
     const size_t slots = (size_t)s.n_det * (size_t)std::max<unsigned long long>(st->n_iv, 1);
-    if (st->ev_val.n < slots || st->ev_pix.n < slots || (c->mode == 0 && st->ev_c1.n < slots)) st->geo_key = 0;
+    const size_t fslots = s.fcache ? (size_t)s.n_species * slots : 1;
+    if (st->ev_val.n < slots || st->ev_pix.n < slots ||
+        (c->mode == 0 && (st->ev_c1.n < slots || st->ev_f.n < fslots)))
+        st->geo_key = 0;
     st->ev_val.grow(slots);
     st->ev_pix.grow(slots);
-    if (c->mode == 0) st->ev_c1.grow(slots);
+    if (c->mode == 0) {
+        st->ev_c1.grow(slots);
+        st->ev_f.grow(fslots);
+    }
     st->lp.grow((size_t)std::max<unsigned long long>(st->n_iv, 1));
     st->own.grow((size_t)std::max<unsigned long long>(st->n_iv, 1));
     ++c->fwd_gen;  // invalidates any cached forward

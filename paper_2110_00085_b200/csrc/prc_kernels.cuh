@@ -45,6 +45,9 @@ struct VertexTable {
     // (geo_ready), which then skip pixel_of, the visibility tests, the phase function and
     // its log.
     int32_t* ev_c1;      // [det][i]
+    // Scenes with DScene::fcache: the phase values f_j(cos_le) of every species as f32,
+    // [j][det][i]; written and read like ev_c1 (both passes use the rounded values).
+    float* ev_f;
     int geo_ready;
 };
 

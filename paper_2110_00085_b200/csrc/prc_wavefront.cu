@@ -207,7 +207,8 @@ __global__ void __launch_bounds__(kWF, kFwdMinBlocks) k_le_forward(const __grid_
     // paths evaluate the same expression, so a recycled image at the sampling point still
     // equals the fresh render.
     const bool c1v = sc.c1_fast && kind == VK_VOLUME;
-    const bool fast = c1v && vt.geo_ready && sc.pad_walk;
+    const bool fv = sc.fcache && kind == VK_VOLUME;  // 2..4 species: cached phase values
+    const bool fast = (c1v || fv) && vt.geo_ready && sc.pad_walk;
     double lvol = -INFINITY;
     if (c1v && live && den > 0.0) {
         const double bt = (double)ea.sp_t[vox];
@@ -224,17 +225,28 @@ __global__ void __launch_bounds__(kWF, kFwdMinBlocks) k_le_forward(const __grid_
         V3 w;
         double r = 0.0, geom = 0.0, logval = -INFINITY;
         if (fast) {
-            if (lvol != -INFINITY) {
-                pix = vt.ev_pix[e];
-                q = vt.ev_c1[e];
-                if (pix >= 0 && q != INT32_MIN) {
-                    // w, r and geom exactly as event_geometry (the walk's indexing is bit-exact)
-                    const V3 to_det = ld3(sc.det[k].pos) - x;
-                    r = norm3(to_det);
-                    w = to_det * (1.0 / r);
-                    geom = 1.0 / (r * r);
-                    logval = lvol + c1_dequant(sc, q);
+            if (c1v) {
+                if (lvol != -INFINITY) {
+                    pix = vt.ev_pix[e];
+                    q = vt.ev_c1[e];
+                    if (pix >= 0 && q != INT32_MIN) logval = lvol + c1_dequant(sc, q);
                 }
+            } else if (live && den > 0.0) {
+                pix = vt.ev_pix[e];
+                if (pix >= 0) {
+                    double num = 0.0;  // scat_num with the cached phase values
+                    for (int j = 0; j < sc.n_species; ++j)
+                        num += sc.sp[j].albedo * (double)ea.sp_t[(long long)j * sc.V + vox] *
+                               (double)vt.ev_f[((unsigned long long)j * sc.n_det + k) * vt.n + i];
+                    if (num > 0.0) logval = lbase + log(num);
+                }
+            }
+            if (logval != -INFINITY) {
+                // w, r and geom exactly as event_geometry (the walk's indexing is bit-exact)
+                const V3 to_det = ld3(sc.det[k].pos) - x;
+                r = norm3(to_det);
+                w = to_det * (1.0 / r);
+                geom = 1.0 / (r * r);
             }
         } else if (act && (live || !vt.geo_ready)) {
             const DDet& D = sc.det[k];
@@ -245,6 +257,14 @@ __global__ void __launch_bounds__(kWF, kFwdMinBlocks) k_le_forward(const __grid_
                 if (c1v) {
                     q = c1_quant(sc, log(sc.sp[0].albedo * phase_eval(sc.sp[0], cos_le)));
                     if (lvol != -INFINITY && q != INT32_MIN) logval = lvol + c1_dequant(sc, q);
+                } else if (fv) {
+                    double num = 0.0;  // scat_num with f32-rounded phase values (as the cache)
+                    for (int j = 0; j < sc.n_species; ++j) {
+                        const float fj = (float)phase_eval(sc.sp[j], cos_le);
+                        if (!vt.geo_ready) vt.ev_f[((unsigned long long)j * sc.n_det + k) * vt.n + i] = fj;
+                        num += sc.sp[j].albedo * (double)ea.sp_t[(long long)j * sc.V + vox] * (double)fj;
+                    }
+                    if (live && num > 0.0 && den > 0.0) logval = lbase + log(num);
                 } else if (kind == VK_VOLUME) {
                     if (live) {
                         const double num = scat_num(sc, ea.sp_t, vox, cos_le);
@@ -491,6 +511,24 @@ __global__ void __launch_bounds__(128, M == 2 ? PRC_GRAD2_MINB : (M == 3 ? PRC_G
                         // pathstore.cpp:97-105), no phase-function evaluations per event
                         const double bt = (double)ea.sp_t[vox];
                         if (bt > 0.0) acc[r] += w / bt;
+                        continue;
+                    }
+                    if (sc.fcache && !ea.legacy) {
+                        // score_term (pathstore.cpp:97-105) from the phase values K4b cached
+                        float fj[kFCacheMax];
+                        double num = 0.0;
+                        for (int j = 0; j < sc.n_species; ++j) {
+                            fj[j] = vt.ev_f[((unsigned long long)j * sc.n_det + k) * vt.n + i];
+                            num += sc.sp[j].albedo * (double)ea.sp_t[(long long)j * sc.V + vox] * (double)fj[j];
+                        }
+                        if (num > 0.0) {
+                            if (single)
+                                acc[r] += w * (sc.sp[sc.unknown].albedo * (double)fj[sc.unknown] / num);
+                            else
+                                for (int j = 0; j < sc.n_species; ++j)
+                                    atomicAdd(ea.g_vert + (long long)j * sc.V + vox,
+                                              w * (sc.sp[j].albedo * (double)fj[j] / num));
+                        }
                         continue;
                     }
                     const double num = ea.legacy ? 0.0 : scat_num(sc, ea.sp_t, vox, cos_le);
