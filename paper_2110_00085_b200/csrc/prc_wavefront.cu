@@ -557,7 +557,6 @@ __global__ void __launch_bounds__(128, M == 2 ? PRC_GRAD2_MINB : (M == 3 ? PRC_G
                 red_add_if(g, same ? -1 : v1, x1);
             }
         } else if (M == 3) {  // hand-scheduled triple (the default packet)
-#ifndef PRC_K5B_VIDX
             PRay R0, R1, R2;
             if (S[0].alive) R0.from(S[0], g, cf[0]); else R0.dead(g);
             if (S[1].alive) R1.from(S[1], g, cf[1]); else R1.dead(g);
@@ -579,24 +578,6 @@ __global__ void __launch_bounds__(128, M == 2 ? PRC_GRAD2_MINB : (M == 3 ? PRC_G
                 red_add_p(e2 && !s20 && !s21, a2, x2);
             };
             while (R0.alive || R1.alive || R2.alive) pstep3();  // (two steps per trip: same time)
-            continue;
-#endif
-            auto step3 = [&]() {
-                double l0, l1, l2;
-                const int v0 = dda_step_pad(S[0], l0);
-                const int v1 = dda_step_pad(S[1], l1);
-                const int v2 = dda_step_pad(S[2], l2);
-                const double x1 = cf[1] * l1, x2 = cf[2] * l2;
-                // dead or zero-length emissions are -1: they only ever match each other,
-                // and emissions at -1 are suppressed, so no validity tests are needed
-                const bool s10 = v1 == v0;
-                const bool s20 = v2 == v0;
-                const bool s21 = v2 == v1 && !s20;
-                red_add_if(g, v0, cf[0] * l0 + (s10 ? x1 : 0.0) + (s20 ? x2 : 0.0));
-                red_add_if(g, s10 ? -1 : v1, x1 + (s21 ? x2 : 0.0));
-                red_add_if(g, (s20 || s21) ? -1 : v2, x2);
-            };
-            while (S[0].alive || S[1].alive || S[2].alive) step3();  // (unrolling x2 measured slower)
         } else if (M == 4) {  // hand-scheduled quad
             while (S[0].alive || S[1].alive || S[2].alive || S[3].alive) {
                 double l0, l1, l2, l3;
