@@ -165,7 +165,7 @@ int prc_gpu_ctx_rank(const prc_gpu_ctx* ctx, int* rank, int* world);
  * species (config (c)); the optimiser still updates the unknown species; "pad" 0 turns
  * off the guard-free walks over the padded voxel layout (default 1; same results);
  * "grad_copies" = copies of the padded gradient the gradient kernel reduces into (0 =
- * default: 4, fewer when they would exceed 2 GB; applied at the next scene upload; same
+ * default: 8, fewer when they would exceed 2 GB; applied at the next scene upload; same
  * results up to the order of floating-point sums). */
 int prc_gpu_ctx_set_option(prc_gpu_ctx* ctx, const char* key, int64_t value);
 

@@ -474,13 +474,14 @@ void upload_scene(prc_gpu_ctx* c, const prc_scene_desc* d) {
         const size_t vpad = c->pad_ok ? (size_t)s.pnxny * (size_t)(s.dims[2] + 2) : 1;
         c->bt_pad.alloc(vpad);
         c->db_pad.alloc(vpad);
-        // copies of the padded gradient for K5b (EvalArgs::g_pad_copies): 4 while they take
-        // at most 2 GB (K5b at 1e8 paths: 784 -> 697 ms at 128^3, 1973 -> 1728 ms at 256^3,
-        // where one copy alone exceeds L2); an explicit "grad_copies" option is taken as given
+        // copies of the padded gradient for K5b (EvalArgs::g_pad_copies): 8 while they take
+        // at most 2 GB (K5b at 1e8 paths: 784 -> 697 ms with 4 copies at 128^3, 670 -> 663 with
+        // 8; 1973 -> 1728 ms with 4 at 256^3, where one copy alone exceeds L2); an explicit
+        // "grad_copies" option is taken as given
         c->g_pad_copies = !(c->pad_ok && vpad > 0) ? 1
                           : c->grad_copies_max > 0
                               ? c->grad_copies_max
-                              : (int)std::max<size_t>(1, std::min<size_t>(4, (size_t(2) << 30) / (vpad * 8)));
+                              : (int)std::max<size_t>(1, std::min<size_t>(8, (size_t(2) << 30) / (vpad * 8)));
         c->g_pad.alloc(vpad * (size_t)c->g_pad_copies);
         CK(cudaMemset(c->bt_pad.p, 0, c->bt_pad.bytes()));  // borders stay zero
         CK(cudaMemset(c->db_pad.p, 0, c->db_pad.bytes()));

@@ -78,8 +78,8 @@ struct EvalArgs {
     // K5b reduces into g_pad_copies copies of the padded gradient, g_pad_stride apart (CTA b
     // into copy b mod copies): same-address reductions from many SMs spread over more L2
     // lines.  Measured at 1e8 paths (config (b)): K5b 784 -> 718 ms with 2 copies, 697 with 4,
-    // 694 with 8; at 256^3 (config (e)) 1973 -> 1808 (2) -> 1728 ms (4).  k_unpad_add sums
-    // the copies; K5a uses copy 0.
+    // 694 with 8; at 256^3 (config (e)) 1973 -> 1808 (2) -> 1728 ms (4).  Default 8 (r13:
+    // 670 -> 663 ms at 128^3).  k_unpad_add sums the copies; K5a uses copy 0.
     long long g_pad_stride;
     int g_pad_copies;
     int per_species, legacy, do_beta;

@@ -1,0 +1,9 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/s8_pytest.log 2>&1; echo pytest=$? >> gpurun_out/s8_pytest.log
+timeout 600 python bench.py > gpurun_out/s8_bench_b.log 2>&1
+timeout 600 python bench.py --config c --steps 3 --warmup 3 --no-e2e > gpurun_out/s8_bench_c.log 2>&1
+timeout 600 python bench.py --config a --no-e2e > gpurun_out/s8_bench_a.log 2>&1
+timeout 600 python bench.py --config d --no-e2e > gpurun_out/s8_bench_d.log 2>&1
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/s8_smoke.log 2>&1
+KERNELS="k_le_gradient_ms k_le_forward" timeout 1800 bash scripts/profile_kernels.sh r11 1e8 > gpurun_out/s8_profile.log 2>&1
+echo done
