@@ -430,6 +430,7 @@ void upload_scene(prc_gpu_ctx* c, const prc_scene_desc* d) {
         }
     }
     s.fcache = s.n_species >= 2 && s.n_species <= kFCacheMax ? 1 : 0;
+    s.scache = s.n_surf > 0 ? 1 : 0;
     // Guard-free walks over the padded layout (prc_device.cuh, dda_walk_pad): exact when
     // the rounding of the tmax sums (~512 ulp of a distance <= 4R) stays far below a voxel.
     if (s.has_medium) {
@@ -680,7 +681,10 @@ void run_forward(prc_gpu_ctx* c, prc_gpu_store* st, const Resolved& r, const Eva
         phong_dev = c->phong.p;
     }
     const size_t slots = (size_t)s.n_det * (size_t)std::max<unsigned long long>(st->n_iv, 1);
-    const size_t fslots = s.fcache ? (size_t)s.n_species * slots : 1;
+    // ev_f: phase values [j][det][i] (fcache), then 8-byte aligned the surface events' f64
+    // cos_le [det][i] (scache); ev_cos_of in prc_wavefront.cu
+    const size_t fslots = std::max<size_t>(
+        1, ((s.fcache ? (size_t)s.n_species * slots : 0) + 1) / 2 * 2 + (s.scache ? 2 * slots : 0));
     if (st->ev_val.n < slots || st->ev_pix.n < slots ||
         (c->mode == 0 && (st->ev_c1.n < slots || st->ev_f.n < fslots)))
         st->geo_key = 0;
@@ -724,8 +728,10 @@ void run_gradient(prc_gpu_ctx* c, prc_gpu_store* st, const EvalArgs& ea) {
     CK(cudaMemsetAsync(c->g_phong.p, 0, 2 * sizeof(double), q));
     if (c->mode == 0) {
         if (s.pad_walk) CK(cudaMemsetAsync(c->g_pad.p, 0, c->g_pad.bytes(), q));
-        CK(launch_le_gradient(s, vertex_table(st), ea, st->own.p, c->spread, s.pad_walk ? c->packet : 1, q,
-                              &c->launches));
+        // lane spreading only de-conflicts the LE-span reductions; without them (no medium,
+        // or no beta gradient) lanes take consecutive vertices so the event loads coalesce
+        CK(launch_le_gradient(s, vertex_table(st), ea, st->own.p, ea.do_beta ? c->spread : 1,
+                              s.pad_walk ? c->packet : 1, q, &c->launches));
         CK(cudaEventRecord(c->ev[7], q));
         c->timed_grad = true;
         CK(launch_path_gradient(s, st->view(), ea, st->own.p, q, &c->launches));

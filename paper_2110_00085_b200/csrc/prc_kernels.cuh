@@ -47,6 +47,10 @@ struct VertexTable {
     int32_t* ev_c1;      // [det][i]
     // Scenes with DScene::fcache: the phase values f_j(cos_le) of every species as f32,
     // [j][det][i]; written and read like ev_c1 (both passes use the rounded values).
+    // Scenes with DScene::scache: each surface event's cos_le as f64, [det][i], stored in
+    // the same buffer after the phase values (ev_cos_of); its geometry factor (f32) is kept
+    // in ev_c1, unused by surface events otherwise.  (One buffer keeps the kernel parameter
+    // layout of medium-only scenes unchanged.)
     float* ev_f;
     int geo_ready;
 };

@@ -179,6 +179,16 @@ __global__ void __launch_bounds__(kTPB) k_prefix(const __grid_constant__ DScene 
 }
 
 // ------------------------------------------------------------------ K4b LE forward
+// VertexTable::ev_f holds [j][det][i] phase values (fcache scenes), then, 8-byte aligned,
+// the [det][i] cos_le of surface events (scache scenes); sized in run_forward (prc_capi.cu).
+__device__ __forceinline__ double* ev_cos_of(const DScene& sc, const VertexTable& vt) {
+    unsigned long long off = sc.fcache ? (unsigned long long)sc.n_species * sc.n_det * vt.n : 0ull;
+    return reinterpret_cast<double*>(vt.ev_f + ((off + 1ull) & ~1ull));
+}
+
+// SC: the scene has surfaces (DScene::scache); the surface-event cache code is compiled
+// only into that instance, so medium-only scenes run the code they ran before it.
+template <bool SC>
 __global__ void __launch_bounds__(kWF, kFwdMinBlocks) k_le_forward(const __grid_constant__ DScene sc,
                                                        const __grid_constant__ VertexTable vt,
                                                        const __grid_constant__ EvalArgs ea,
@@ -208,12 +218,17 @@ __global__ void __launch_bounds__(kWF, kFwdMinBlocks) k_le_forward(const __grid_
     // equals the fresh render.
     const bool c1v = sc.c1_fast && kind == VK_VOLUME;
     const bool fv = sc.fcache && kind == VK_VOLUME;  // 2..4 species: cached phase values
-    const bool fast = (c1v || fv) && vt.geo_ready && sc.pad_walk;
+    const bool sv = SC && kind == VK_SURFACE;       // cached cos_le and geometry factor
+    const bool fast = vt.geo_ready && (((c1v || fv) && sc.pad_walk) || sv);
     double lvol = -INFINITY;
     if (c1v && live && den > 0.0) {
         const double bt = (double)ea.sp_t[vox];
         if (bt > 0.0) lvol = lbase + log(bt);
     }
+    // Cached surface events without a medium: when |lp| < 300 and 1e-100 <= f_r <= 1e100 the
+    // log value stays inside the clamp range, so exp(lp + log f_r) is taken as e^lp * f_r
+    // (one exp per vertex instead of a log and an exp per event; ~1e-16 relative)
+    const double elp = (sv && live && fast && !sc.has_medium && fabs(lpv) < 300.0) ? exp(lpv) : 0.0;
     unsigned clamps = 0;
     for (int k = 0; k < sc.n_det; ++k) {
         const unsigned long long e = (unsigned long long)k * vt.n + i;
@@ -223,9 +238,24 @@ __global__ void __launch_bounds__(kWF, kFwdMinBlocks) k_le_forward(const __grid_
         int pix = -1;
         int32_t q = INT32_MIN;
         V3 w;
-        double r = 0.0, geom = 0.0, logval = -INFINITY;
+        double r = 0.0, geom = 0.0, logval = -INFINITY, direct = 0.0;
         if (fast) {
-            if (c1v) {
+            if (sv) {
+                if (live) {
+                    pix = vt.ev_pix[e];
+                    if (pix >= 0) {
+                        const double fr = surf_brdf(sc, ea.phong, surf, ev_cos_of(sc, vt)[e]);
+                        if (fr > 0.0) {
+                            if (elp != 0.0 && fr >= 1e-100 && fr <= 1e100) {
+                                direct = elp * fr;
+                                geom = (double)__int_as_float(vt.ev_c1[e]);
+                            } else {
+                                logval = lpv + log(fr);
+                            }
+                        }
+                    }
+                }
+            } else if (c1v) {
                 if (lvol != -INFINITY) {
                     pix = vt.ev_pix[e];
                     q = vt.ev_c1[e];
@@ -242,11 +272,14 @@ __global__ void __launch_bounds__(kWF, kFwdMinBlocks) k_le_forward(const __grid_
                 }
             }
             if (logval != -INFINITY) {
-                // w, r and geom exactly as event_geometry (the walk's indexing is bit-exact)
-                const V3 to_det = ld3(sc.det[k].pos) - x;
-                r = norm3(to_det);
-                w = to_det * (1.0 / r);
-                geom = 1.0 / (r * r);
+                // w, r and geom exactly as event_geometry (the walk's indexing is bit-exact);
+                // a cached surface event needs the ray only for the LE walk
+                if (!sv || sc.has_medium) {
+                    const V3 to_det = ld3(sc.det[k].pos) - x;
+                    r = norm3(to_det);
+                    w = to_det * (1.0 / r);
+                }
+                geom = sv ? (double)__int_as_float(vt.ev_c1[e]) : 1.0 / (r * r);
             }
         } else if (act && (live || !vt.geo_ready)) {
             const DDet& D = sc.det[k];
@@ -270,16 +303,27 @@ __global__ void __launch_bounds__(kWF, kFwdMinBlocks) k_le_forward(const __grid_
                         const double num = scat_num(sc, ea.sp_t, vox, cos_le);
                         if (num > 0.0 && den > 0.0) logval = lbase + log(num);
                     }
-                } else if (live) {
-                    const double fr = surf_brdf(sc, ea.phong, surf, cos_le);
-                    if (fr > 0.0) logval = lpv + log(fr);
+                } else {
+                    if (sv) {  // cached for later passes; both passes use the f32 geometry factor
+                        geom = (double)(float)geom;
+                        q = __float_as_int((float)geom);
+                        if (!vt.geo_ready) ev_cos_of(sc, vt)[e] = cos_le;
+                    }
+                    if (live) {
+                        const double fr = surf_brdf(sc, ea.phong, surf, cos_le);
+                        if (fr > 0.0) logval = lpv + log(fr);
+                    }
                 }
             } else {
                 pix = -1;
             }
         }
         float val = 0.0f;
-        if (logval != -INFINITY) {
+        if (SC && direct != 0.0) {
+            const double contrib = direct * geom * sc.prefactor;
+            val = (float)contrib;
+            if (contrib != 0.0) atomicAdd(ea.images + sc.det[k].img_off + pix, contrib);
+        } else if (logval != -INFINITY) {
             if (sc.has_medium) {
                 logval -= sc.pad_walk ? dda_optical_depth_pad(sc, x, w, r, ea.bt_pad)
                                       : dda_optical_depth(sc, x, w, r, ea.bt_tot);
@@ -313,6 +357,26 @@ __device__ __forceinline__ double score_j(const DScene& sc, const EvalArgs& ea, 
         return bt > 0.0 ? 1.0 / bt : 0.0;
     }
     return num > 0.0 ? sc.sp[j].albedo * phase_eval(sc.sp[j], c) / num : 0.0;
+}
+
+// The gradient passes' event geometry: surface events of DScene::scache scenes take cos_le
+// from the per-store cache K4b wrote (and w, r as event_geometry computes them); the rest
+// recompute it.  Only events with a value reach here, so the visibility test has passed.
+template <bool SC>
+__device__ __forceinline__ void grad_event_geometry(const DScene& sc, const VertexTable& vt, const EvalArgs& ea,
+                                                    int k, unsigned long long i, V3 x, V3 d, uint32_t kind,
+                                                    int surf, V3& w, double& r, double& cos_le) {
+    if (SC && vt.geo_ready && kind == VK_SURFACE) {
+        if (ea.do_beta) {  // the LE walk's ray
+            const V3 to_det = ld3(sc.det[k].pos) - x;
+            r = norm3(to_det);
+            w = to_det * (1.0 / r);
+        }
+        cos_le = ev_cos_of(sc, vt)[(unsigned long long)k * vt.n + i];
+        return;
+    }
+    double geom;
+    event_geometry(sc, sc.det[k], x, d, kind, surf, w, r, geom, cos_le);
 }
 
 // One LE ray per thread, one fp64 L2 reduction per voxel visit (packet = 1).  Lane
@@ -355,8 +419,8 @@ __global__ void __launch_bounds__(kWF, PRC_GRAD1_MINB) k_le_gradient(const __gri
         own_acc += w;
         const V3 x = mk(vt.x[i], vt.y[i], vt.z[i]);
         V3 wd;
-        double r, geom, cos_le;
-        event_geometry(sc, sc.det[k], x, mk(vt.dx[i], vt.dy[i], vt.dz[i]), kind, surf, wd, r, geom, cos_le);
+        double r, cos_le;
+        grad_event_geometry<true>(sc, vt, ea, k, i, x, mk(vt.dx[i], vt.dy[i], vt.dz[i]), kind, surf, wd, r, cos_le);
         if (ea.do_beta) {
             const double cf = -w;
             if (sc.pad_walk) {
@@ -460,7 +524,7 @@ __device__ __forceinline__ void red_add_p(bool e, double* a, double x) {
 // (~0.39 per voxel visit for M = 3 at 1e8 paths: the reference DDA on the bench geometry
 // gives 0.53 / 0.39 / 0.31 for M = 2 / 3 / 4 vertices in a 0.3-voxel cube), while `spread` keeps the 32 lanes of a
 // warp on distinct packets far apart in Morton order (no same-address RED conflicts).
-template <int M>
+template <int M, bool SC>
 __global__ void __launch_bounds__(128, M == 2 ? PRC_GRAD2_MINB : (M == 3 ? PRC_GRAD3_MINB : PRC_GRAD4_MINB)) k_le_gradient_ms(const __grid_constant__ DScene sc,
                                                         const __grid_constant__ VertexTable vt,
                                                         const __grid_constant__ EvalArgs ea,
@@ -499,8 +563,8 @@ __global__ void __launch_bounds__(128, M == 2 ? PRC_GRAD2_MINB : (M == 3 ? PRC_G
             const uint32_t kind = meta_kind(meta);
             const int surf = meta_surface(meta);
             V3 wd;
-            double rr, geom, cos_le;
-            event_geometry(sc, sc.det[k], x, d, kind, surf, wd, rr, geom, cos_le);
+            double rr, cos_le;
+            grad_event_geometry<SC>(sc, vt, ea, k, i, x, d, kind, surf, wd, rr, cos_le);
             if (ea.do_beta) {
                 S[r].init<true>(sc, x, wd, rr);  // packets run on the padded layout only
                 cf[r] = -w;
@@ -809,7 +873,10 @@ cudaError_t launch_prefix(const DScene& sc, const StoreView& st, const EvalArgs&
 cudaError_t launch_le_forward(const DScene& sc, const VertexTable& vt, const EvalArgs& ea,
                               const double* lp, cudaStream_t s, unsigned long long* launches) {
     if (vt.n == 0) return cudaSuccess;
-    k_le_forward<<<grid_for((long long)vt.n, kWF), kWF, 0, s>>>(sc, vt, ea, lp);
+    if (sc.scache)
+        k_le_forward<true><<<grid_for((long long)vt.n, kWF), kWF, 0, s>>>(sc, vt, ea, lp);
+    else
+        k_le_forward<false><<<grid_for((long long)vt.n, kWF), kWF, 0, s>>>(sc, vt, ea, lp);
     LAUNCH_DONE();
 }
 
@@ -819,11 +886,14 @@ cudaError_t launch_le_gradient(const DScene& sc, const VertexTable& vt, const Ev
     if (packet > 1) {
         const long long n_pk = ((long long)vt.n + packet - 1) / packet;
         if (packet == 2)
-            k_le_gradient_ms<2><<<grid_for(n_pk, 128), 128, 0, s>>>(sc, vt, ea, own, spread);
+            (sc.scache ? k_le_gradient_ms<2, true> : k_le_gradient_ms<2, false>)<<<grid_for(n_pk, 128), 128, 0, s>>>(
+                sc, vt, ea, own, spread);
         else if (packet == 3)
-            k_le_gradient_ms<3><<<grid_for(n_pk, 128), 128, 0, s>>>(sc, vt, ea, own, spread);
+            (sc.scache ? k_le_gradient_ms<3, true> : k_le_gradient_ms<3, false>)<<<grid_for(n_pk, 128), 128, 0, s>>>(
+                sc, vt, ea, own, spread);
         else
-            k_le_gradient_ms<4><<<grid_for(n_pk, 128), 128, 0, s>>>(sc, vt, ea, own, spread);
+            (sc.scache ? k_le_gradient_ms<4, true> : k_le_gradient_ms<4, false>)<<<grid_for(n_pk, 128), 128, 0, s>>>(
+                sc, vt, ea, own, spread);
         LAUNCH_DONE();
     }
     k_le_gradient<<<grid_for((long long)vt.n, kWF), kWF, 0, s>>>(sc, vt, ea, own, spread);

@@ -618,6 +618,33 @@ def test_event_geometry_cache_follows_the_cameras(ctx, golden_dir):
         assert grad_err(r.grad_beta, ref.grad_beta) <= 1e-12
 
 
+@pytest.mark.parametrize("name", ["phong", "mixed"])
+def test_surface_event_cache_reuse(ctx, golden_dir, name):
+    """Scenes with surfaces: the first forward over a store caches each surface event's
+    pixel, cos_le and geometry factor; later forwards and gradients (other kappa/gamma or
+    beta) read them instead of redoing pixel_of and the visibility tests. Cached passes
+    equal the pass that wrote the cache, and the reference's values at every point."""
+    scene = FIXTURES[name]["scene"]()
+    g = golden(name)
+    w = weight_patterns(scene)["w"]
+    p = perturbed(scene)
+    ctx.upload(scene)
+    st = ctx.load_store(str(golden_dir / f"{name}.pstr"))
+    first = ctx.evaluate_store(scene, st, p, EvalOptions(want_grad=True, pixel_weights=w))
+    ctx.evaluate_store(scene, st, None, EvalOptions())  # another point in between
+    again = ctx.evaluate_store(scene, st, p, EvalOptions(want_grad=True, pixel_weights=w))
+    assert img_err(again.images, first.images) <= 1e-12
+    assert img_err(again.images, g["pert_w_images"]) <= IMG_TOL
+    if scene.unknown_species() >= 0:
+        assert grad_err(again.grad_beta, first.grad_beta) <= 1e-12
+        assert grad_err(again.grad_beta, g["pert_w_grad"]) <= GRAD_TOL
+    else:
+        assert scalar_err(again.grad_kappa, first.grad_kappa) <= 1e-12
+        assert scalar_err(again.grad_gamma, first.grad_gamma) <= 1e-12
+        assert scalar_err(again.grad_kappa, float(g["pert_w_gk"])) <= GRAD_TOL
+        assert scalar_err(again.grad_gamma, float(g["pert_w_gg"])) <= GRAD_TOL
+
+
 def test_gradient_copies_option_same_results(ctx, golden_dir):
     """K5b's reductions into 1 or 4 copies of the padded gradient give the same gradient
     up to the order of floating-point sums."""
