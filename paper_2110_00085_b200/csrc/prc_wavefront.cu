@@ -6,7 +6,7 @@
 //
 //   K4a k_prefix        thread per path, B-sorted store (Path Sorting): incoming-segment
 //                       log-prefix at every interaction vertex -> lp[iv]
-//   K4b k_le_forward    CTA per run of Morton-ordered interaction vertices, camera by
+//   K4b k_le_forward    CTA per run of 128 Morton-ordered interaction vertices, camera by
 //                       camera: LE transmittance, event value, image scatter, event cache
 //   K5b k_le_gradient_ms<3>  same vertex order: w = value * residual, LE scatter -w*l
 //                       with fp64 L2 reductions (three rays per thread in lockstep, spans
@@ -28,15 +28,20 @@ using namespace prc;
 namespace {
 
 constexpr int kWF = 256;  // vertices per CTA in the wavefront kernels
+#ifndef PRC_FWD_TPB
+#define PRC_FWD_TPB 128
+#endif
+constexpr int kFwdTPB = PRC_FWD_TPB;  // K4b: vertices per CTA (128 x 8 CTAs 379.6 ms vs 256 x 4 382.3)
 constexpr int kTPB = 128;
 // Occupancy (measured on B200 at 1e8 paths, config (b)).  K4b with the guarded walk: 6
 // CTAs x 256 threads (40 registers) 604 ms vs 5 CTAs 613, 4 CTAs 639, 3 CTAs 714; with
 // the padded, software-pipelined walk: 5 CTAs (48 registers) 449 ms vs 6 CTAs 458; with
 // four steps per trip: 4 CTAs (64 registers) 411 ms vs 5 CTAs 430, 6 CTAs 876.  K5b
 // packet-3 at 4 CTAs x 128 threads (128 registers) 937 ms vs 3 CTAs 977, 2 CTAs 977, 5
-// CTAs 1102; packet 2 (4 CTAs) 1108, packet 4 (3 CTAs) 1132.
+// CTAs 1102; packet 2 (4 CTAs) 1108, packet 4 (3 CTAs) 1132.  K4b at 64 registers in
+// smaller CTAs (r15): 8 x 128 threads 379.6 ms vs 4 x 256 382.3, 2 x 512 391.4, 7 x 128 394.9.
 #ifndef PRC_FWD_MINB  // -D overrides are for A/B builds (scripts/variants_lib.sh)
-#define PRC_FWD_MINB 4
+#define PRC_FWD_MINB 8
 #endif
 #ifndef PRC_GRAD1_MINB
 #define PRC_GRAD1_MINB 3
@@ -189,11 +194,11 @@ __device__ __forceinline__ double* ev_cos_of(const DScene& sc, const VertexTable
 // SC: the scene has surfaces (DScene::scache); the surface-event cache code is compiled
 // only into that instance, so medium-only scenes run the code they ran before it.
 template <bool SC>
-__global__ void __launch_bounds__(kWF, kFwdMinBlocks) k_le_forward(const __grid_constant__ DScene sc,
+__global__ void __launch_bounds__(kFwdTPB, kFwdMinBlocks) k_le_forward(const __grid_constant__ DScene sc,
                                                        const __grid_constant__ VertexTable vt,
                                                        const __grid_constant__ EvalArgs ea,
                                                        const double* __restrict__ lp) {
-    const unsigned long long i = (unsigned long long)blockIdx.x * kWF + threadIdx.x;
+    const unsigned long long i = (unsigned long long)blockIdx.x * kFwdTPB + threadIdx.x;
     const bool act = i < vt.n;
     int vox = 0;
     uint32_t meta = 0;
@@ -874,9 +879,9 @@ cudaError_t launch_le_forward(const DScene& sc, const VertexTable& vt, const Eva
                               const double* lp, cudaStream_t s, unsigned long long* launches) {
     if (vt.n == 0) return cudaSuccess;
     if (sc.scache)
-        k_le_forward<true><<<grid_for((long long)vt.n, kWF), kWF, 0, s>>>(sc, vt, ea, lp);
+        k_le_forward<true><<<grid_for((long long)vt.n, kFwdTPB), kFwdTPB, 0, s>>>(sc, vt, ea, lp);
     else
-        k_le_forward<false><<<grid_for((long long)vt.n, kWF), kWF, 0, s>>>(sc, vt, ea, lp);
+        k_le_forward<false><<<grid_for((long long)vt.n, kFwdTPB), kFwdTPB, 0, s>>>(sc, vt, ea, lp);
     LAUNCH_DONE();
 }
 
