@@ -32,7 +32,14 @@ constexpr int kWF = 256;  // vertices per CTA in the wavefront kernels
 #define PRC_FWD_TPB 128
 #endif
 constexpr int kFwdTPB = PRC_FWD_TPB;  // K4b: vertices per CTA (128 x 8 CTAs 379.6 ms vs 256 x 4 382.3)
-constexpr int kTPB = 128;
+#ifndef PRC_PATH_TPB
+#define PRC_PATH_TPB 128
+#endif
+#ifndef PRC_GRAD_TPB
+#define PRC_GRAD_TPB 128
+#endif
+constexpr int kTPB = PRC_PATH_TPB;   // thread-per-path kernels (K4a, K5a, vertex keys)
+constexpr int kGradTPB = PRC_GRAD_TPB;  // K5b packets per CTA
 // Occupancy (measured on B200 at 1e8 paths, config (b)).  K4b with the guarded walk: 6
 // CTAs x 256 threads (40 registers) 604 ms vs 5 CTAs 613, 4 CTAs 639, 3 CTAs 714; with
 // the padded, software-pipelined walk: 5 CTAs (48 registers) 449 ms vs 6 CTAs 458; with
@@ -530,7 +537,7 @@ __device__ __forceinline__ void red_add_p(bool e, double* a, double x) {
 // gives 0.53 / 0.39 / 0.31 for M = 2 / 3 / 4 vertices in a 0.3-voxel cube), while `spread` keeps the 32 lanes of a
 // warp on distinct packets far apart in Morton order (no same-address RED conflicts).
 template <int M, bool SC>
-__global__ void __launch_bounds__(128, M == 2 ? PRC_GRAD2_MINB : (M == 3 ? PRC_GRAD3_MINB : PRC_GRAD4_MINB)) k_le_gradient_ms(const __grid_constant__ DScene sc,
+__global__ void __launch_bounds__(kGradTPB, M == 2 ? PRC_GRAD2_MINB : (M == 3 ? PRC_GRAD3_MINB : PRC_GRAD4_MINB)) k_le_gradient_ms(const __grid_constant__ DScene sc,
                                                         const __grid_constant__ VertexTable vt,
                                                         const __grid_constant__ EvalArgs ea,
                                                         double* __restrict__ own, int spread) {
@@ -891,13 +898,13 @@ cudaError_t launch_le_gradient(const DScene& sc, const VertexTable& vt, const Ev
     if (packet > 1) {
         const long long n_pk = ((long long)vt.n + packet - 1) / packet;
         if (packet == 2)
-            (sc.scache ? k_le_gradient_ms<2, true> : k_le_gradient_ms<2, false>)<<<grid_for(n_pk, 128), 128, 0, s>>>(
+            (sc.scache ? k_le_gradient_ms<2, true> : k_le_gradient_ms<2, false>)<<<grid_for(n_pk, kGradTPB), kGradTPB, 0, s>>>(
                 sc, vt, ea, own, spread);
         else if (packet == 3)
-            (sc.scache ? k_le_gradient_ms<3, true> : k_le_gradient_ms<3, false>)<<<grid_for(n_pk, 128), 128, 0, s>>>(
+            (sc.scache ? k_le_gradient_ms<3, true> : k_le_gradient_ms<3, false>)<<<grid_for(n_pk, kGradTPB), kGradTPB, 0, s>>>(
                 sc, vt, ea, own, spread);
         else
-            (sc.scache ? k_le_gradient_ms<4, true> : k_le_gradient_ms<4, false>)<<<grid_for(n_pk, 128), 128, 0, s>>>(
+            (sc.scache ? k_le_gradient_ms<4, true> : k_le_gradient_ms<4, false>)<<<grid_for(n_pk, kGradTPB), kGradTPB, 0, s>>>(
                 sc, vt, ea, own, spread);
         LAUNCH_DONE();
     }
