@@ -134,7 +134,12 @@ __global__ void k_vt_gather(const __grid_constant__ StoreView st, const uint32_t
 // regeneration used by K5a is slower here, because a K4a step is only a gather + FMA.)
 __device__ __forceinline__ int warp_count(bool p) { return __popc(__ballot_sync(0xffffffffu, p)); }
 
-__global__ void __launch_bounds__(kTPB) k_prefix(const __grid_constant__ DScene sc,
+#ifdef PRC_PREFIX_MINB  // A/B: occupancy of K4a
+#define PRC_PREFIX_LB __launch_bounds__(kTPB, PRC_PREFIX_MINB)
+#else
+#define PRC_PREFIX_LB __launch_bounds__(kTPB)
+#endif
+__global__ void PRC_PREFIX_LB k_prefix(const __grid_constant__ DScene sc,
                                                  const __grid_constant__ StoreView st,
                                                  const __grid_constant__ EvalArgs ea, double* lp) {
     const long long p = path_index(st.n);
@@ -732,7 +737,13 @@ __global__ void __launch_bounds__(kGradTPB, M == 2 ? PRC_GRAD2_MINB : (M == 3 ? 
 // from_here = W - prefix (suffix sums of pathstore.cpp:219-237 from own[iv]) weights the
 // incoming segment's spans; continuation score terms use after = W - prefix_next.
 template <bool PAD>
-__global__ void __launch_bounds__(kTPB) k_path_gradient(const __grid_constant__ DScene sc,
+// K5a occupancy (r15b, 1e8 paths): 6 CTAs x 128 (85 registers) 49.3 ms vs 5 CTAs (95
+// registers, no bound) 53.2, 8 CTAs 53.0
+#ifndef PRC_PATHG_MINB
+#define PRC_PATHG_MINB 6
+#endif
+#define PRC_PATHG_LB __launch_bounds__(kTPB, PRC_PATHG_MINB)
+__global__ void PRC_PATHG_LB k_path_gradient(const __grid_constant__ DScene sc,
                                                         const __grid_constant__ StoreView st,
                                                         const __grid_constant__ EvalArgs ea,
                                                         const double* __restrict__ own) {
