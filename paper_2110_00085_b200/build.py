@@ -38,20 +38,22 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str = OUT
     if out == OUT and not defines and not force and not _stale():
         return OUT
     tag = "" if out == OUT else "." + os.path.basename(out).replace(".so", "")
-    objs = []
-    for s in SOURCES:
+    objs, procs = [], []
+    for s in SOURCES:  # the translation units compile in parallel
         obj = os.path.join(SRC if not tag else os.path.dirname(out), s.replace(".cu", tag + ".o"))
         cmd = [NVCC, *FLAGS, *("-D" + d for d in defines), "-c", os.path.join(SRC, s), "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        if r.returncode != 0:
-            sys.stderr.write(r.stdout + r.stderr)
+        procs.append((s, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
+        objs.append(obj)
+    for s, p in procs:
+        so, se = p.communicate()
+        if p.returncode != 0:
+            sys.stderr.write(so + se)
             raise RuntimeError(f"nvcc failed on {s}")
         if verbose:
-            sys.stderr.write(r.stderr)
+            sys.stderr.write(se)
         if not tag:  # register / spill report (compile times dropped: the file is tracked)
             with open(os.path.join(SRC, s.replace(".cu", ".ptxas.txt")), "w") as f:
-                f.write("".join(l for l in r.stderr.splitlines(True) if "Compile time" not in l))
-        objs.append(obj)
+                f.write("".join(l for l in se.splitlines(True) if "Compile time" not in l))
     tmp = out + ".tmp"
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs,
            "-lnccl", "-Xlinker", "-rpath,/usr/lib/x86_64-linux-gnu"]

@@ -146,6 +146,9 @@ struct prc_gpu_ctx {
     // bumped whenever cameras, scene or options change: invalidates every store's cached
     // event geometry (prc_gpu_store::geo_key)
     unsigned long long geo_gen = 1;
+    // bumped by every scene upload: a store whose reference-side tables (br_tot64, sp_ref,
+    // br_tot) were built under another upload rebuilds them before use (store_for_scene)
+    unsigned long long scene_gen = 0;
     unsigned long long last_fwd_gen = ~0ull, last_fwd_key = 0;
     const prc_gpu_store* last_fwd_store = nullptr;
     unsigned long long last_fwd_clamps = 0;
@@ -155,7 +158,7 @@ struct prc_gpu_ctx {
     double last_ms[8] = {};
     std::set<prc_gpu_store*> stores;  // live stores made by this context (orphaned on destroy)
     int g_pad_copies = 1;  // see EvalArgs::g_pad_copies
-    int grad_copies_max = 0;  // option "grad_copies" (applied at scene upload); 0: 4
+    int grad_copies_max = 0;  // option "grad_copies" (applied at scene upload); 0: 8 while <= 2 GB
     ~prc_gpu_ctx() {
         if (cub_tmp) cudaFree(cub_tmp);
         for (auto& e : timer)
@@ -207,6 +210,10 @@ struct prc_gpu_store {
     std::vector<double> ref_beta;
     double ref_kappa = 0.0, ref_gamma = 0.0;
     unsigned long long segments = 0, truncated = 0;
+    // scene the store was built or last re-bound under (store_for_scene)
+    unsigned long long scene_gen = 0;
+    int dims[3] = {0, 0, 0};
+    int n_species = 0;
 
     prc_gpu_store() = default;
     explicit prc_gpu_store(prc_gpu_ctx* c) : ctx(c), device(c->device) { c->stores.insert(this); }
@@ -314,6 +321,7 @@ long long finalize_detectors(DScene& s, const prc_detector_desc* dd, int n, cons
 }
 
 void upload_scene(prc_gpu_ctx* c, const prc_scene_desc* d) {
+    ++c->scene_gen;
     ++c->geo_gen;  // cameras / species / surfaces may change: cached event geometry is stale
     ++c->fwd_gen;  // and so is a cached forward (grad_forward after recycled_render)
     if (d->n_species < 0 || d->n_species > PRC_MAX_SPECIES)
@@ -543,6 +551,38 @@ Resolved resolve_params(prc_gpu_ctx* c, const prc_gpu_params* p, const prc_gpu_s
         r.gamma = p->gamma;
     }
     return r;
+}
+
+// Stamps a store with the current scene (trace / import).
+void stamp_store(prc_gpu_ctx* c, prc_gpu_store* st) {
+    st->scene_gen = c->scene_gen;
+    for (int a = 0; a < 3; ++a) st->dims[a] = c->dsc.dims[a];
+    st->n_species = c->dsc.n_species;
+}
+
+// Reference-side tables of a store for the scene on the device.  make_context
+// (pathstore.cpp:41-82) rebuilds the reference side from the current scene and the
+// store's ref_params on every call; the store caches it per scene upload.  A store built
+// under another grid cannot be evaluated (its voxel ids index that grid).
+void store_for_scene(prc_gpu_ctx* c, prc_gpu_store* st) {
+    const DScene& s = c->dsc;
+    if (st->n_species != s.n_species || st->dims[0] != s.dims[0] || st->dims[1] != s.dims[1] ||
+        st->dims[2] != s.dims[2])
+        throw Err(PRC_ERR_INVALID, "the store was built for a different grid or species set than the uploaded scene");
+    if (st->scene_gen == c->scene_gen) return;
+    const long long V = c->V;
+    const double* src[PRC_MAX_SPECIES] = {};
+    for (int j = 0; j < s.n_species; ++j) src[j] = c->scene_sp.p + (size_t)j * V;
+    if (s.unknown >= 0 && !st->ref_beta.empty()) {
+        if ((long long)st->ref_beta.size() != V) throw Err(PRC_ERR_INVALID, "store reference beta size != voxel count");
+        c->trace_sp.grow((size_t)V);
+        CK(cudaMemcpyAsync(c->trace_sp.p, st->ref_beta.data(), (size_t)V * 8, cudaMemcpyHostToDevice, c->stream));
+        src[s.unknown] = c->trace_sp.p;
+    }
+    CK(launch_prep_ref(s.n_species, V, src, st->br_tot64.p, st->sp_ref.p, st->br_tot.p, nullptr, c->stream,
+                       &c->launches));
+    c->sync();
+    st->scene_gen = c->scene_gen;
 }
 
 // 64-bit content hash of the evaluated parameters (forward-reuse key).
@@ -791,6 +831,7 @@ std::unique_ptr<prc_gpu_store> trace_store(prc_gpu_ctx* c, const prc_gpu_render_
     const DScene& s = c->dsc;
     cudaStream_t q = c->stream;
     auto st = std::make_unique<prc_gpu_store>(c);
+    stamp_store(c, st.get());
     const unsigned long long N = o->n_paths;
     st->n_global = N;
     st->stream_base = N * (unsigned long long)c->rank / (unsigned long long)c->world;
@@ -911,13 +952,12 @@ void sort_store(prc_gpu_ctx* c, prc_gpu_store* st) {
     DBuf<uint32_t> perm;
     perm.alloc((size_t)n);
     CK(launch_sort_rank(st->B.p, n, nb, tile, toff.p, perm.p, q, &c->launches));
-    // bucket table: start of bin k = toff[k * n_tiles]
-    std::vector<unsigned long long> all((size_t)nb * n_tiles);
-    CK(cudaMemcpyAsync(all.data(), toff.p, all.size() * sizeof(unsigned long long),
-                       cudaMemcpyDeviceToHost, q));
-    c->sync();
+    // bucket table: start of bin k = toff[k * n_tiles] (one strided copy of column 0)
     std::vector<unsigned long long> bstart(nb + 1), brec(nb + 1), biv(nb + 1);
-    for (int k = 0; k < nb; ++k) bstart[k] = all[(size_t)k * n_tiles];
+    CK(cudaMemcpy2DAsync(bstart.data(), sizeof(unsigned long long), toff.p,
+                         (size_t)n_tiles * sizeof(unsigned long long), sizeof(unsigned long long), (size_t)nb,
+                         cudaMemcpyDeviceToHost, q));
+    c->sync();
     bstart[nb] = (unsigned long long)n;
     unsigned long long R = 0, I = 0;
     for (int k = 0; k <= nb; ++k) {
@@ -1194,6 +1234,7 @@ std::unique_ptr<prc_gpu_store> import_pstr(prc_gpu_ctx* c, const std::string& pa
         throw Err(PRC_ERR_IO, "load_store: bad magic at offset 0 in " + path);
     if (get<uint32_t>(is) != 1) throw Err(PRC_ERR_IO, "load_store: unsupported version");
     auto st = std::make_unique<prc_gpu_store>(c);
+    stamp_store(c, st.get());
     const uint64_t count = get<uint64_t>(is);
     st->generation = get<uint64_t>(is);
     st->seed = get<uint64_t>(is);
@@ -1249,6 +1290,9 @@ std::unique_ptr<prc_gpu_store> import_pstr(prc_gpu_ctx* c, const std::string& pa
             const int8_t spc = get<int8_t>(is);
             const uint8_t kind = get<uint8_t>(is);
             if (!mine) continue;
+            // the kernels index the grid with stored voxel ids: range-check them
+            if (vx < -1 || (long long)vx >= c->V || (kind == VK_VOLUME && vx < 0))
+                throw Err(PRC_ERR_IO, "load_store: vertex voxel index outside the uploaded grid in " + path);
             // incoming direction: dir0 for the first segment, the chord direction after
             H3 d = d0;
             double t = 0.0;
@@ -1550,6 +1594,8 @@ PRC_EXPORT int prc_gpu_store_export_pstr(prc_gpu_ctx* ctx, const prc_gpu_store* 
     if (store->ctx != ctx) return fail(PRC_ERR_INVALID, "prc_gpu_store_export_pstr: the store belongs to another context");
     ABI_TRY
     begin(ctx);
+    ctx->check_scene();
+    store_for_scene(ctx, const_cast<prc_gpu_store*>(store));
     export_pstr(ctx, const_cast<prc_gpu_store*>(store), path);
     ABI_CATCH
 }
@@ -1589,6 +1635,7 @@ PRC_EXPORT int prc_gpu_evaluate(prc_gpu_ctx* ctx, const prc_gpu_store* store,
     begin(ctx);
     ctx->check_scene();
     auto* st = const_cast<prc_gpu_store*>(store);
+    store_for_scene(ctx, st);
     EvalRun er;
     er.want_grad = (flags & PRC_EVAL_WANT_GRAD) != 0;
     er.per_species = (flags & PRC_EVAL_PER_SPECIES) != 0;
@@ -1760,6 +1807,8 @@ PRC_EXPORT int prc_gpu_opt_step(prc_gpu_ctx* ctx, const prc_gpu_store* store, do
     if (store->ctx != ctx) return fail(PRC_ERR_INVALID, "prc_gpu_opt_step: the store belongs to another context");
     ABI_TRY
     begin(ctx);
+    ctx->check_scene();
+    store_for_scene(ctx, const_cast<prc_gpu_store*>(store));
     const double l = opt_step(ctx, const_cast<prc_gpu_store*>(store));
     if (loss_out) *loss_out = l;
     ABI_CATCH
@@ -1957,7 +2006,10 @@ PRC_EXPORT int prc_gpu_reconstruct_schedule(prc_gpu_ctx* ctx, const prc_gpu_para
     std::vector<prc_gpu_iteration_log> rows;
     std::vector<double> loss_hist;
     const int n_r = std::max(1, sch->recycle_period);
-    const int w = sch->saturation_window > 0 ? sch->saturation_window : 20;
+    // inverse.cpp:249-258 takes the window as given (0 advances at the first check); a
+    // negative window would index past the loss history there, so it is rejected here
+    if (sch->saturation_window < 0) throw Err(PRC_ERR_CONFIG, "reconstruct: saturation_window must be >= 0");
+    const int w = sch->saturation_window;
     const double rel = sch->saturation_rel_improvement;
     int stage = 0, applied = -1, pending = 0, stage_start = 0;
     uint64_t phases = 0, truncated = 0;
@@ -2179,6 +2231,7 @@ PRC_EXPORT int prc_gpu_store_stats(prc_gpu_ctx* ctx, const prc_gpu_store* store,
     ABI_TRY
     begin(ctx);
     ctx->check_scene();
+    store_for_scene(ctx, const_cast<prc_gpu_store*>(store));
     DBuf<unsigned long long> d;
     d.alloc(4);
     CK(cudaMemsetAsync(d.p, 0, 32, ctx->stream));

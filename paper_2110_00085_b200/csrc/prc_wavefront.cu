@@ -583,7 +583,7 @@ __global__ void __launch_bounds__(kGradTPB, M == 2 ? PRC_GRAD2_MINB : (M == 3 ? 
             double rr, cos_le;
             grad_event_geometry<SC>(sc, vt, ea, k, i, x, d, kind, surf, wd, rr, cos_le);
             if (ea.do_beta) {
-                S[r].init<true>(sc, x, wd, rr);  // packets run on the padded layout only
+                S[r].template init<true>(sc, x, wd, rr);  // packets run on the padded layout only
                 cf[r] = -w;
                 if (kind == VK_VOLUME) {
                     const int vox = vt.vox[i];
@@ -648,7 +648,8 @@ __global__ void __launch_bounds__(kGradTPB, M == 2 ? PRC_GRAD2_MINB : (M == 3 ? 
                 const bool e0 = R0.step(x0, a0);
                 const bool e1 = R1.step(x1, a1);
                 const bool e2 = R2.step(x2, a2);
-                // same voxel <=> same address; the table is < 4 GB, so the low 32 bits decide
+                // same voxel <=> same address; launch_le_gradient runs this packet only on
+                // padded tables below 2^29 voxels (4 GB), so the low 32 bits decide
                 const uint32_t l0 = (uint32_t)(uintptr_t)a0, l1 = (uint32_t)(uintptr_t)a1,
                                l2 = (uint32_t)(uintptr_t)a2;
                 const bool s10 = e0 && e1 && l1 == l0;
@@ -737,8 +738,9 @@ __global__ void __launch_bounds__(kGradTPB, M == 2 ? PRC_GRAD2_MINB : (M == 3 ? 
 // from_here = W - prefix (suffix sums of pathstore.cpp:219-237 from own[iv]) weights the
 // incoming segment's spans; continuation score terms use after = W - prefix_next.
 template <bool PAD>
-// K5a occupancy (r15b, 1e8 paths): 6 CTAs x 128 (85 registers) 49.3 ms vs 5 CTAs (95
-// registers, no bound) 53.2, 8 CTAs 53.0
+// K5a occupancy (r15b, 1e8 paths): 6 CTAs x 128 (80 registers, with 112-138 B of spills
+// per thread accepted: prc_wavefront.ptxas.txt) 49.3 ms vs 5 CTAs (95 registers, no bound)
+// 53.2, 8 CTAs 53.0
 #ifndef PRC_PATHG_MINB
 #define PRC_PATHG_MINB 6
 #endif
@@ -906,6 +908,9 @@ cudaError_t launch_le_forward(const DScene& sc, const VertexTable& vt, const Eva
 cudaError_t launch_le_gradient(const DScene& sc, const VertexTable& vt, const EvalArgs& ea, double* own,
                                int spread, int packet, cudaStream_t s, unsigned long long* launches) {
     if (vt.n == 0) return cudaSuccess;
+    // the packet-3 merge compares the low 32 bits of table addresses: exact below 2^29
+    // padded voxels (4 GB per copy); larger tables take packet 2 (int voxel compares)
+    if (packet == 3 && (long long)sc.pnxny * (long long)(sc.dims[2] + 2) >= (1ll << 29)) packet = 2;
     if (packet > 1) {
         const long long n_pk = ((long long)vt.n + packet - 1) / packet;
         if (packet == 2)

@@ -683,3 +683,52 @@ def test_store_outlives_its_context(golden_dir):
     finally:
         a.close()
         b.close()
+
+
+def test_store_rejects_a_scene_with_another_grid(ctx, golden_dir):
+    """A store's voxel ids index the grid it was built under; evaluating it against a
+    scene with another grid is refused instead of reading out of bounds."""
+    from paper_2110_00085_b200.gpu import PrcInvalidError
+    scene = FIXTURES["cloud"]["scene"]()
+    ctx.upload(scene)
+    st = ctx.load_store(str(golden_dir / "cloud.pstr"))
+    other = S.cloud_scene(8, 10, 10)
+    with pytest.raises(PrcInvalidError):
+        ctx.evaluate_store(other, st, None, EvalOptions())
+    ctx.upload(scene)
+    assert ctx.evaluate_store(scene, st, None, EvalOptions()).images.sum() > 0
+
+
+def test_store_reference_side_follows_the_scene(ctx, ref, golden_dir):
+    """make_context (pathstore.cpp:41-82) builds the reference side of every known
+    species from the current scene on each call.  A re-uploaded scene whose known species
+    changed must therefore change the store's reference tables too."""
+    scene = FIXTURES["tomo2"]["scene"]()
+    ctx.upload(scene)
+    st = ctx.load_store(str(golden_dir / "tomo2.pstr"))
+    ctx.evaluate_store(scene, st, None, EvalOptions())
+    s2 = FIXTURES["tomo2"]["scene"]()
+    s2.species[1].extinction = s2.species[1].extinction * 1.3  # the known species
+    w = weight_patterns(s2)["w"]
+    p = perturbed(s2)
+    r = ctx.evaluate_store(s2, st, p, EvalOptions(want_grad=True, pixel_weights=w))
+    e = ref.evaluate(s2, str(golden_dir / "tomo2.pstr"), p, abi.PRC_EVAL_NORMALIZE | abi.PRC_EVAL_WANT_GRAD, w)
+    assert img_err(r.images, e["images"]) <= IMG_TOL
+    assert grad_err(r.grad_beta, e["grad"]) <= GRAD_TOL
+
+
+def test_import_range_checks_voxel_ids(ctx, golden_dir, tmp_path):
+    """load_store: a vertex voxel id outside the uploaded grid is an I/O error, not an
+    out-of-bounds gather in the kernels."""
+    import struct
+    scene = FIXTURES["cloud"]["scene"]()
+    ctx.upload(scene)
+    raw = bytearray((golden_dir / "cloud.pstr").read_bytes())
+    nb = struct.unpack_from("<Q", raw, 33)[0]
+    rec0 = 41 + 8 * nb + 16
+    vox_at = rec0 + 8 + 1 + 24 + 4 + 56  # record 0, vertex 0, VertexRec::voxel
+    struct.pack_into("<i", raw, vox_at, scene.voxel_count + 5)
+    bad = tmp_path / "bad_vox.pstr"
+    bad.write_bytes(bytes(raw))
+    with pytest.raises(PrcIOError, match="voxel"):
+        ctx.load_store(str(bad))
