@@ -395,6 +395,19 @@ def main():
     ap.add_argument("--packet", type=int, default=None, help="K5b rays per thread in lockstep")
     ap.add_argument("--grad-copies", type=int, default=None, help="max copies of the padded gradient K5b reduces into")
     args = ap.parse_args()
+    world_env = os.environ.get("WORLD_SIZE")
+    if world_env is not None and int(world_env) != args.gpus:
+        sys.exit(f"bench.py: WORLD_SIZE={world_env} but --gpus {args.gpus}")
+    if world_env is None and args.gpus > 1 and args.impl == "ours":
+        # one process per GPU: re-launch this command under torch.distributed.run
+        import socket
+        sock = socket.socket()
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+        sock.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -153,8 +153,15 @@ int prc_gpu_ctx_create(int device, prc_gpu_ctx** out);
  * 128-byte ncclUniqueId produced by prc_gpu_nccl_unique_id on rank 0 and broadcast
  * by the caller (e.g. through torch.distributed). */
 int prc_gpu_nccl_unique_id(void* out128);
+/* nccl_id NULL with world > 1: a detached shard without a communicator.  The context
+ * traces / imports rank `rank`'s stream range and every result it returns (images,
+ * gradients, clamp and truncation counts) is that shard's partial sum, still normalised by
+ * the global path count; the caller reduces them (e.g. over MPI or torch.distributed). */
 int prc_gpu_ctx_create_rank(int device, int rank, int world, const void* nccl_id,
                             prc_gpu_ctx** out);
+/* The contiguous stream range [lo, hi) rank `rank` of `world` owns out of n paths
+ * (floor(n r / w) .. floor(n (r+1) / w)).  Host-only, no device needed. */
+int prc_gpu_shard_range(uint64_t n, int rank, int world, uint64_t* lo, uint64_t* hi);
 void prc_gpu_ctx_destroy(prc_gpu_ctx* ctx);
 int prc_gpu_ctx_rank(const prc_gpu_ctx* ctx, int* rank, int* world);
 /* Engine knobs: "mode" 0 = event-major wavefront over Morton-ordered interaction
@@ -210,6 +217,7 @@ typedef struct {
     int sorted;
     int max_size;              /* max B */
     uint64_t device_bytes;     /* device memory held by the store */
+    int materialized;          /* imported with PRC_IMPORT_MATERIALIZE */
 } prc_gpu_store_info;
 
 int prc_gpu_store_info_get(const prc_gpu_store* store, prc_gpu_store_info* out);
@@ -221,6 +229,15 @@ int prc_gpu_store_sizes(const prc_gpu_store* store, uint32_t* out);
  * event on the device.  Import accepts reference-written files. */
 int prc_gpu_store_export_pstr(prc_gpu_ctx* ctx, const prc_gpu_store* store, const char* path);
 int prc_gpu_store_import_pstr(prc_gpu_ctx* ctx, const char* path, prc_gpu_store** out);
+/* load_store with options.  PRC_IMPORT_MATERIALIZE keeps the file's own segment spans,
+ * events and LE spans on the device and evaluates them as eval_record reads them
+ * (pathstore.cpp:115-238): the reference's voxel ids and span lengths, fp64 throughout.
+ * Without it (prc_gpu_store_import_pstr) spans are recomputed by the DDA along chord
+ * directions (voxel ids identical, lengths within rounding) and the store runs on the
+ * recycling kernels.  A materialized store exports its records verbatim (sorted:
+ * in storage order), byte-identical to the reference's save_store of the same store. */
+enum { PRC_IMPORT_MATERIALIZE = 1 };
+int prc_gpu_store_import_pstr_ex(prc_gpu_ctx* ctx, const char* path, int flags, prc_gpu_store** out);
 int prc_gpu_store_set_generation(prc_gpu_store* store, uint64_t generation);
 /* A store belongs to the context that made it: passing it with another context returns
  * PRC_ERR_INVALID.  prc_gpu_store_free is valid before or after that context is destroyed

@@ -212,6 +212,7 @@ class Reference:
         L.ref_render_json.argtypes = [C.c_char_p, C.c_uint64, C.c_uint64, _dp, C.c_uint64]
         L.ref_save_pfm.argtypes = [C.c_char_p, C.c_int, C.c_int, _dp]
         L.ref_load_pfm.argtypes = [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int), _dp, C.c_uint64]
+        L.ref_segment_lengths.argtypes = [C.c_void_p, C.c_char_p, _u64p, _u32p, _u32p, _dp]
 
     def _err(self):
         return self.lib.ref_last_error().decode()
@@ -278,6 +279,21 @@ class Reference:
             raise ValueError(self._err())
         return dict(images=img, grad=grad[:scene.voxel_count], grad_kappa=gk.value,
                     grad_gamma=gg.value, clamp_events=int(cl.value), mean_correction=mc.value)
+
+    def segment_lengths(self, scene: Scene, pstr: str):
+        """segment_lengths (pathstore.cpp:296-313) of every record: (counts per segment, voxels,
+        lengths), records in file order, segments b = 1..B."""
+        h = scene.desc()
+        sz = np.zeros(2, np.uint64)
+        if self.lib.ref_segment_lengths(h.ptr, pstr.encode(), _ptr(sz, _u64p), None, None, None):
+            raise ValueError(self._err())
+        counts = np.zeros(max(int(sz[0]), 1), np.uint32)
+        vox = np.zeros(max(int(sz[1]), 1), np.uint32)
+        ln = np.zeros(max(int(sz[1]), 1))
+        if self.lib.ref_segment_lengths(h.ptr, pstr.encode(), _ptr(sz, _u64p), _ptr(counts, _u32p),
+                                        _ptr(vox, _u32p), _ptr(ln, _dp)):
+            raise ValueError(self._err())
+        return counts[:int(sz[0])], vox[:int(sz[1])], ln[:int(sz[1])]
 
     def time_iteration(self, scene: Scene, ref: Optional[ParamSet], t: ParamSet, n: int, seed: int,
                        workers: int, reps: int = 1, warmup: int = 0) -> dict:

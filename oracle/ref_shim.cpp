@@ -256,6 +256,36 @@ int ref_evaluate(const prc_scene_desc* d, const char* pstr, const prc_gpu_params
     }
 }
 
+/* segment_lengths (pathstore.cpp:296-313) of every record of a PSTR file, records in file
+ * order, segments b = 1..B: counts[k] spans of segment k; vox/len receive them
+ * concatenated.  sizes_out[0] = segments, [1] = spans (call with counts = NULL first). */
+int ref_segment_lengths(const prc_scene_desc* d, const char* pstr, uint64_t* sizes_out, uint32_t* counts,
+                        uint32_t* vox, double* len) {
+    try {
+        Scene s = make_scene(d);
+        PathStore st = load_store(pstr);
+        uint64_t k = 0, m = 0;
+        for (const auto& rec : st.records) {
+            for (const auto& seg : segment_lengths(rec, *s.grid())) {
+                if (counts) counts[k] = static_cast<uint32_t>(seg.spans.size());
+                for (const auto& sp : seg.spans) {
+                    if (vox) {
+                        vox[m] = sp.voxel;
+                        len[m] = sp.length;
+                    }
+                    ++m;
+                }
+                ++k;
+            }
+        }
+        sizes_out[0] = k;
+        sizes_out[1] = m;
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
 /* CPU baseline: render(keep) + sort, then `warmup` untimed and `reps` timed recycled iterations
  * (recycled_render + residual + grad_forward) at params t with `workers` threads.
  * stats[0]=segments S, [1]=trace s, [2]=sort s, [3]=mean forward s, [4]=mean grad s,

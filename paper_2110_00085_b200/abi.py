@@ -15,6 +15,7 @@ PRC_EVAL_WANT_GRAD = 2
 PRC_EVAL_LEGACY_SCORE = 4
 PRC_EVAL_SELF_NORMALIZE = 8
 PRC_EVAL_PER_SPECIES = 16
+PRC_IMPORT_MATERIALIZE = 1
 
 c_double_p = C.POINTER(C.c_double)
 
@@ -68,7 +69,7 @@ class StoreInfo(C.Structure):
                 ("stream_base", C.c_uint64), ("segments", C.c_uint64), ("vertices", C.c_uint64),
                 ("interaction_vertices", C.c_uint64), ("truncated", C.c_uint64),
                 ("seed", C.c_uint64), ("generation", C.c_uint64), ("sorted", C.c_int),
-                ("max_size", C.c_int), ("device_bytes", C.c_uint64)]
+                ("max_size", C.c_int), ("device_bytes", C.c_uint64), ("materialized", C.c_int)]
 
 
 class EvalOpts(C.Structure):

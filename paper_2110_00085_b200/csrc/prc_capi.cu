@@ -214,6 +214,19 @@ struct prc_gpu_store {
     unsigned long long scene_gen = 0;
     int dims[3] = {0, 0, 0};
     int n_species = 0;
+    // Materialized imports (prc_gpu_store_import_pstr_ex with PRC_IMPORT_MATERIALIZE): the
+    // file's own spans / events on the device (MatView, prc_materialized.cu) and its raw
+    // record bytes on the host (export writes them back verbatim).
+    bool mat = false;
+    std::vector<char> mat_bytes;
+    std::vector<size_t> mat_off;  // record r = mat_bytes[mat_off[r], mat_off[r + 1])
+    DBuf<unsigned long long> m_rec, m_vbase, m_sbase, m_ebase, m_lbase;
+    DBuf<uint32_t> m_vmeta, m_vsb, m_vse, m_svox, m_evert, m_esb, m_ese, m_lvox;
+    DBuf<int32_t> m_vvox, m_edet, m_epix;
+    DBuf<double> m_vct, m_slen, m_ecos, m_egeom, m_llen, m_eval;
+    DBuf<double> m_ref64, m_bt, m_br, m_db;  // fp64 context of make_context
+    unsigned long long m_events = 0;
+    MatCtx m_ctx{};
 
     prc_gpu_store() = default;
     explicit prc_gpu_store(prc_gpu_ctx* c) : ctx(c), device(c->device) { c->stores.insert(this); }
@@ -261,8 +274,42 @@ struct prc_gpu_store {
     RecordsOut rec_out() {
         return RecordsOut{px.p, py.p, pz.p, dx.p, dy.p, dz.p, tt.p, ct.p, vox.p, meta.p};
     }
+    MatView mat_view() {
+        MatView v{};
+        v.n = n;
+        v.rec = m_rec.p;
+        v.v_base = m_vbase.p;
+        v.s_base = m_sbase.p;
+        v.e_base = m_ebase.p;
+        v.l_base = m_lbase.p;
+        v.v_meta = m_vmeta.p;
+        v.v_vox = m_vvox.p;
+        v.v_ct = m_vct.p;
+        v.v_sb = m_vsb.p;
+        v.v_se = m_vse.p;
+        v.s_vox = m_svox.p;
+        v.s_len = m_slen.p;
+        v.e_vert = m_evert.p;
+        v.e_det = m_edet.p;
+        v.e_pix = m_epix.p;
+        v.e_cos = m_ecos.p;
+        v.e_geom = m_egeom.p;
+        v.e_sb = m_esb.p;
+        v.e_se = m_ese.p;
+        v.l_vox = m_lvox.p;
+        v.l_len = m_llen.p;
+        v.e_val = m_eval.p;
+        return v;
+    }
+    unsigned long long mat_device_bytes() const {
+        return m_rec.bytes() + m_vbase.bytes() + m_sbase.bytes() + m_ebase.bytes() + m_lbase.bytes() +
+               m_vmeta.bytes() + m_vsb.bytes() + m_vse.bytes() + m_svox.bytes() + m_evert.bytes() + m_esb.bytes() +
+               m_ese.bytes() + m_lvox.bytes() + m_vvox.bytes() + m_edet.bytes() + m_epix.bytes() + m_vct.bytes() +
+               m_slen.bytes() + m_ecos.bytes() + m_egeom.bytes() + m_llen.bytes() + m_eval.bytes() +
+               m_ref64.bytes() + m_bt.bytes() + m_br.bytes() + m_db.bytes();
+    }
     unsigned long long device_bytes() const {
-        return B.bytes() + stride.bytes() + stream.bytes() + rec_base.bytes() + iv_base.bytes() +
+        return mat_device_bytes() + B.bytes() + stride.bytes() + stream.bytes() + rec_base.bytes() + iv_base.bytes() +
                trunc.bytes() + px.bytes() * 8 + vox.bytes() + meta.bytes() + ev_val.bytes() +
                ev_pix.bytes() + ev_c1.bytes() + ev_f.bytes() + br_tot64.bytes() + sp_ref.bytes() + br_tot.bytes() + lp.bytes() +
                own.bytes() + vt_x.bytes() * 6 + vt_vox.bytes() + vt_meta.bytes() + vt_iv.bytes();
@@ -270,6 +317,14 @@ struct prc_gpu_store {
 };
 
 namespace {
+
+// Contiguous stream range [lo, hi) of rank r among w: floor(N r / w) ..
+// floor(N (r + 1) / w), exact in 128-bit arithmetic; the ranges of all ranks partition
+// [0, N) and differ in size by at most one.
+void shard_range(unsigned long long N, int r, int w, unsigned long long* lo, unsigned long long* hi) {
+    *lo = (unsigned long long)((unsigned __int128)N * (unsigned)r / (unsigned)w);
+    *hi = (unsigned long long)((unsigned __int128)N * (unsigned)(r + 1) / (unsigned)w);
+}
 
 int fail(int code, const std::string& m) {
     g_last_error = m;
@@ -560,6 +615,26 @@ void stamp_store(prc_gpu_ctx* c, prc_gpu_store* st) {
     st->n_species = c->dsc.n_species;
 }
 
+// fp64 reference species values of a materialized store (make_context's ref side,
+// pathstore.cpp:54-61): the scene's values, the unknown species' from ref_params.beta.
+void mat_ref_tables(prc_gpu_ctx* c, prc_gpu_store* st) {
+    const DScene& s = c->dsc;
+    const long long V = c->V;
+    const size_t nsV = (size_t)std::max(1, s.n_species) * (size_t)std::max<long long>(V, 1);
+    st->m_ref64.alloc(nsV);
+    st->m_bt.alloc((size_t)std::max<long long>(V, 1));
+    st->m_br.alloc((size_t)std::max<long long>(V, 1));
+    st->m_db.alloc((size_t)std::max<long long>(V, 1));
+    if (s.n_species > 0 && V > 0) {
+        CK(cudaMemcpyAsync(st->m_ref64.p, c->scene_sp.p, (size_t)s.n_species * V * 8, cudaMemcpyDeviceToDevice,
+                           c->stream));
+        if (s.unknown >= 0 && !st->ref_beta.empty())
+            CK(cudaMemcpyAsync(st->m_ref64.p + (size_t)s.unknown * V, st->ref_beta.data(), (size_t)V * 8,
+                               cudaMemcpyHostToDevice, c->stream));
+    }
+    c->sync();
+}
+
 // Reference-side tables of a store for the scene on the device.  make_context
 // (pathstore.cpp:41-82) rebuilds the reference side from the current scene and the
 // store's ref_params on every call; the store caches it per scene upload.  A store built
@@ -582,6 +657,7 @@ void store_for_scene(prc_gpu_ctx* c, prc_gpu_store* st) {
     CK(launch_prep_ref(s.n_species, V, src, st->br_tot64.p, st->sp_ref.p, st->br_tot.p, nullptr, c->stream,
                        &c->launches));
     c->sync();
+    if (st->mat) mat_ref_tables(c, st);
     st->scene_gen = c->scene_gen;
 }
 
@@ -720,6 +796,32 @@ void run_forward(prc_gpu_ctx* c, prc_gpu_store* st, const Resolved& r, const Eva
         CK(cudaMemcpyAsync(c->phong.p, ph, sizeof ph, cudaMemcpyHostToDevice, q));
         phong_dev = c->phong.p;
     }
+    if (st->mat) {  // stored spans (prc_materialized.cu)
+        if (!phong_dev) {
+            const double ph[2] = {r.kappa, r.gamma};
+            CK(cudaMemcpyAsync(c->phong.p, ph, sizeof ph, cudaMemcpyHostToDevice, q));
+            phong_dev = c->phong.p;
+        }
+        for (int j = 0; j < PRC_MAX_SPECIES; ++j) st->m_ctx.t[j] = r.src[j];
+        st->m_ctx.ref = st->m_ref64.p;
+        st->m_ctx.bt_tot = st->m_bt.p;
+        st->m_ctx.br_tot = st->m_br.p;
+        st->m_ctx.dbeta = st->m_db.p;
+        CK(launch_mat_prep(s.n_species, c->V, st->m_ctx, q, &c->launches));
+        ++c->fwd_gen;
+        CK(cudaMemsetAsync(c->images.p, 0, c->images.bytes(), q));
+        CK(cudaMemsetAsync(c->clamps.p, 0, sizeof(unsigned long long), q));
+        CK(cudaMemsetAsync(st->m_eval.p, 0, st->m_eval.bytes(), q));
+        ea = eval_args(c, st, er, phong_dev);
+        c->timed_sub = c->timed_grad = false;
+        CK(cudaEventRecord(c->ev[1], q));
+        CK(launch_mat_forward(s, st->mat_view(), st->m_ctx, ea, q, &c->launches));
+        CK(cudaEventRecord(c->ev[2], q));
+        c->allreduce(c->images.p, (size_t)c->n_pix);
+        c->allreduce_u64(c->clamps.p, 1);
+        CK(cudaEventRecord(c->ev[3], q));
+        return;
+    }
     const size_t slots = (size_t)s.n_det * (size_t)std::max<unsigned long long>(st->n_iv, 1);
     // ev_f: phase values [j][det][i] (fcache), then 8-byte aligned the surface events' f64
     // cos_le [det][i] (scache); ev_cos_of in prc_wavefront.cu
@@ -766,7 +868,9 @@ void run_gradient(prc_gpu_ctx* c, prc_gpu_store* st, const EvalArgs& ea) {
     CK(cudaMemsetAsync(c->g_span.p, 0, c->g_span.bytes(), q));
     CK(cudaMemsetAsync(c->g_vert.p, 0, c->g_vert.bytes(), q));
     CK(cudaMemsetAsync(c->g_phong.p, 0, 2 * sizeof(double), q));
-    if (c->mode == 0) {
+    if (st->mat) {
+        CK(launch_mat_gradient(s, st->mat_view(), st->m_ctx, ea, q, &c->launches));
+    } else if (c->mode == 0) {
         if (s.pad_walk) CK(cudaMemsetAsync(c->g_pad.p, 0, c->g_pad.bytes(), q));
         // lane spreading only de-conflicts the LE-span reductions; without them (no medium,
         // or no beta gradient) lanes take consecutive vertices so the event loads coalesce
@@ -834,8 +938,8 @@ std::unique_ptr<prc_gpu_store> trace_store(prc_gpu_ctx* c, const prc_gpu_render_
     stamp_store(c, st.get());
     const unsigned long long N = o->n_paths;
     st->n_global = N;
-    st->stream_base = N * (unsigned long long)c->rank / (unsigned long long)c->world;
-    const unsigned long long end = N * (unsigned long long)(c->rank + 1) / (unsigned long long)c->world;
+    unsigned long long end = 0;
+    shard_range(N, c->rank, c->world, &st->stream_base, &end);
     st->n = end - st->stream_base;
     st->seed = o->seed;
     st->ref_kappa = kappa;
@@ -1006,6 +1110,13 @@ void sort_store(prc_gpu_ctx* c, prc_gpu_store* st) {
                            &c->launches));
     CK(cudaMemcpyAsync(st->vox.p, half0, st->n_rec * 4, cudaMemcpyDeviceToDevice, q));
     CK(cudaMemcpyAsync(st->meta.p, half1, st->n_rec * 4, cudaMemcpyDeviceToDevice, q));
+    if (st->mat) {  // storage position -> file record of a materialized store
+        DBuf<unsigned long long> nr;
+        nr.alloc((size_t)n);
+        CK(launch_gather_u64(perm.p, n, st->m_rec.p, nr.p, q, &c->launches));
+        c->sync();
+        st->m_rec.swap(nr);
+    }
     c->sync();
     st->B.swap(ns->B);
     st->stream.swap(ns->stream);
@@ -1037,7 +1148,32 @@ std::vector<T> d2h(const DBuf<T>& b, size_t n, cudaStream_t q) {
     return h;
 }
 
+// save_store of a materialized store: the header from the store, then the file's own
+// record bytes in storage order (so a sorted store writes what sort_by_size + save_store
+// of the reference writes, pathstore.cpp:261-267, 410-453).
+void export_materialized(prc_gpu_ctx* c, prc_gpu_store* st, const std::string& path) {
+    std::vector<unsigned long long> rec(st->n);
+    if (st->n) CK(cudaMemcpyAsync(rec.data(), st->m_rec.p, st->n * 8, cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    std::ofstream os(path, std::ios::binary);
+    if (!os) throw Err(PRC_ERR_IO, "save_store: cannot open " + path);
+    os.write("PSTR", 4);
+    put<uint32_t>(os, 1u);
+    put<uint64_t>(os, st->n);
+    put<uint64_t>(os, st->generation);
+    put<uint64_t>(os, st->seed);
+    put<uint8_t>(os, st->sorted ? 1 : 0);
+    put<uint64_t>(os, st->ref_beta.size());
+    for (double b : st->ref_beta) put<double>(os, b);
+    put<double>(os, st->ref_kappa);
+    put<double>(os, st->ref_gamma);
+    for (unsigned long long r : rec)
+        os.write(st->mat_bytes.data() + st->mat_off[r], (std::streamsize)(st->mat_off[r + 1] - st->mat_off[r]));
+    if (!os) throw Err(PRC_ERR_IO, "save_store: write failure on " + path);
+}
+
 void export_pstr(prc_gpu_ctx* c, prc_gpu_store* st, const std::string& path) {
+    if (st->mat) return export_materialized(c, st, path);
     const DScene& s = c->dsc;
     cudaStream_t q = c->stream;
     const unsigned long long n = st->n;
@@ -1224,7 +1360,15 @@ void export_pstr(prc_gpu_ctx* c, prc_gpu_store* st, const std::string& path) {
     if (!os) throw Err(PRC_ERR_IO, "save_store: write failure on " + path);
 }
 
-std::unique_ptr<prc_gpu_store> import_pstr(prc_gpu_ctx* c, const std::string& path) {
+// Host arrays of the stored spans / events of a materialized import (MatView).
+struct MatHost {
+    std::vector<unsigned long long> vbase{0}, sbase, ebase{0}, lbase;
+    std::vector<uint32_t> vmeta, vsb, vse, svox, evert, esb, ese, lvox;
+    std::vector<int32_t> vvox, edet, epix;
+    std::vector<double> vct, slen, ecos, egeom, llen;
+};
+
+std::unique_ptr<prc_gpu_store> import_pstr(prc_gpu_ctx* c, const std::string& path, bool materialize) {
     const DScene& s = c->dsc;
     std::ifstream is(path, std::ios::binary);
     if (!is) throw Err(PRC_ERR_IO, "load_store: cannot open " + path);
@@ -1248,8 +1392,8 @@ std::unique_ptr<prc_gpu_store> import_pstr(prc_gpu_ctx* c, const std::string& pa
     if (s.unknown >= 0 && !st->ref_beta.empty() && (long long)nb != c->V)
         throw Err(PRC_ERR_CONFIG, "load_store: reference beta size != voxel count");
     // this rank's slice of the records
-    const uint64_t lo = count * (uint64_t)c->rank / (uint64_t)c->world;
-    const uint64_t hi = count * (uint64_t)(c->rank + 1) / (uint64_t)c->world;
+    unsigned long long lo = 0, hi = 0;
+    shard_range(count, c->rank, c->world, &lo, &hi);
     st->n_global = count;
     st->stream_base = lo;
     st->n = hi - lo;
@@ -1261,7 +1405,11 @@ std::unique_ptr<prc_gpu_store> import_pstr(prc_gpu_ctx* c, const std::string& pa
     std::vector<uint32_t> meta;
     unsigned long long n_iv = 0;
     int maxB = 0;
+    MatHost mh;
+    st->mat = materialize;
+    if (materialize) st->mat_off.push_back(0);
     for (uint64_t i = 0; i < count; ++i) {
+        const std::streampos rec_start = is.tellg();
         const uint64_t stream = get<uint64_t>(is);
         const uint8_t tr = get<uint8_t>(is);
         H3 d0{get<double>(is), get<double>(is), get<double>(is)};
@@ -1278,13 +1426,14 @@ std::unique_ptr<prc_gpu_store> import_pstr(prc_gpu_ctx* c, const std::string& pa
             n_iv += nv >= 3 ? nv - 2 : 0;
             maxB = std::max(maxB, (int)nv - 1);
         }
+        const bool keep = materialize && mine;
         for (uint32_t k = 0; k < nv; ++k) {
             H3 x{get<double>(is), get<double>(is), get<double>(is)};
             const double cth = get<double>(is);
             (void)get<double>(is);  // cos_in (not on the recycling path)
             (void)get<double>(is);  // cos_out
-            (void)get<uint32_t>(is);
-            (void)get<uint32_t>(is);
+            const uint32_t vsb = get<uint32_t>(is);
+            const uint32_t vse = get<uint32_t>(is);
             const int32_t vx = get<int32_t>(is);
             const int16_t sf = get<int16_t>(is);
             const int8_t spc = get<int8_t>(is);
@@ -1293,13 +1442,18 @@ std::unique_ptr<prc_gpu_store> import_pstr(prc_gpu_ctx* c, const std::string& pa
             // the kernels index the grid with stored voxel ids: range-check them
             if (vx < -1 || (long long)vx >= c->V || (kind == VK_VOLUME && vx < 0))
                 throw Err(PRC_ERR_IO, "load_store: vertex voxel index outside the uploaded grid in " + path);
-            // incoming direction: dir0 for the first segment, the chord direction after
+            // incoming direction: dir0 for the first segment, the chord direction after,
+            // formed as the reference's segment_lengths does, d * (1.0 / len)
+            // (pathstore.cpp:300-311), so the re-walk is that function's walk bit for bit
             H3 d = d0;
             double t = 0.0;
             if (k >= 1) {
                 const H3 ch = hsub(x, prev);
                 t = hnorm(ch);
-                d = k == 1 ? d0 : (t > 0.0 ? hnormalized(ch) : pdir);
+                if (k >= 2) {
+                    const double inv = 1.0 / t;
+                    d = t > 0.0 ? H3{ch.x * inv, ch.y * inv, ch.z * inv} : pdir;
+                }
             }
             px.push_back(x.x);
             py.push_back(x.y);
@@ -1312,16 +1466,89 @@ std::unique_ptr<prc_gpu_store> import_pstr(prc_gpu_ctx* c, const std::string& pa
             vox.push_back(vx);
             meta.push_back((uint32_t)(kind & 0xffu) | ((uint32_t)(uint8_t)spc << 8) |
                            ((uint32_t)(uint16_t)sf << 16));
+            if (keep) {
+                mh.vmeta.push_back(meta.back());
+                mh.vvox.push_back(vx);
+                mh.vct.push_back(cth);
+                mh.vsb.push_back(vsb);
+                mh.vse.push_back(vse);
+            }
             prev = x;
             pdir = d;
         }
-        // spans, events and LE spans are recomputed on the device: skip them
-        uint32_t ns = get<uint32_t>(is);
-        is.seekg((std::streamoff)ns * 12, std::ios::cur);
-        uint32_t ne = get<uint32_t>(is);
-        is.seekg((std::streamoff)ne * 34, std::ios::cur);
-        uint32_t nl = get<uint32_t>(is);
-        is.seekg((std::streamoff)nl * 12, std::ios::cur);
+        if (!keep) {  // spans, events and LE spans are recomputed on the device: skip them
+            uint32_t ns = get<uint32_t>(is);
+            is.seekg((std::streamoff)ns * 12, std::ios::cur);
+            uint32_t ne = get<uint32_t>(is);
+            is.seekg((std::streamoff)ne * 34, std::ios::cur);
+            uint32_t nl = get<uint32_t>(is);
+            is.seekg((std::streamoff)nl * 12, std::ios::cur);
+            if (!is) throw Err(PRC_ERR_IO, "load_store: truncated file " + path);
+            continue;
+        }
+        // materialized: the stored spans and events as eval_record reads them, range-checked
+        // against the uploaded scene (pathstore.cpp:455-516 reads them unchecked)
+        auto bad = [&](const char* what) {
+            return Err(PRC_ERR_IO, std::string("load_store: ") + what + " in record " + std::to_string(i) + " of " + path);
+        };
+        const uint32_t ns = get<uint32_t>(is);
+        mh.sbase.push_back(mh.svox.size());
+        for (uint32_t k = 0; k < ns; ++k) {
+            const uint32_t v = get<uint32_t>(is);
+            const double l = get<double>(is);
+            if ((long long)v >= c->V) throw bad("span voxel outside the uploaded grid");
+            mh.svox.push_back(v);
+            mh.slen.push_back(l);
+        }
+        for (uint32_t k = 0; k < nv; ++k) {
+            const size_t vi = mh.vsb.size() - nv + k;
+            if (mh.vsb[vi] > mh.vse[vi] || mh.vse[vi] > ns) throw bad("vertex span range outside the record");
+        }
+        const uint32_t ne = get<uint32_t>(is);
+        std::vector<uint32_t> ese_tmp;
+        for (uint32_t k = 0; k < ne; ++k) {
+            const uint32_t vb = get<uint32_t>(is);
+            const uint16_t det = get<uint16_t>(is);
+            const int32_t pix = get<int32_t>(is);
+            const double cl = get<double>(is);
+            const double gm = get<double>(is);
+            const uint32_t eb = get<uint32_t>(is);
+            const uint32_t ee = get<uint32_t>(is);
+            if (vb >= nv) throw bad("event vertex outside the path");
+            if (det >= s.n_det || pix < 0 || (long long)pix >= (long long)s.det[det].rows * s.det[det].cols)
+                throw bad("event detector / pixel outside the uploaded cameras");
+            if (eb > ee) throw bad("event span range reversed");
+            mh.evert.push_back(vb);
+            mh.edet.push_back(det);
+            mh.epix.push_back(pix);
+            mh.ecos.push_back(cl);
+            mh.egeom.push_back(gm);
+            mh.esb.push_back(eb);
+            mh.ese.push_back(ee);
+            ese_tmp.push_back(ee);
+        }
+        mh.ebase.push_back(mh.evert.size());
+        const uint32_t nl = get<uint32_t>(is);
+        for (uint32_t e : ese_tmp)
+            if (e > nl) throw bad("event span range outside the record");
+        mh.lbase.push_back(mh.lvox.size());
+        for (uint32_t k = 0; k < nl; ++k) {
+            const uint32_t v = get<uint32_t>(is);
+            const double l = get<double>(is);
+            if ((long long)v >= c->V) throw bad("LE span voxel outside the uploaded grid");
+            mh.lvox.push_back(v);
+            mh.llen.push_back(l);
+        }
+        mh.vbase.push_back(mh.vmeta.size());
+        if (!is) throw Err(PRC_ERR_IO, "load_store: truncated file " + path);
+        // raw record bytes for a verbatim export
+        const std::streampos rec_end = is.tellg();
+        const size_t len = (size_t)(rec_end - rec_start);
+        const size_t at = st->mat_bytes.size();
+        st->mat_bytes.resize(at + len);
+        is.seekg(rec_start);
+        is.read(st->mat_bytes.data() + at, (std::streamsize)len);
+        st->mat_off.push_back(st->mat_bytes.size());
         if (!is) throw Err(PRC_ERR_IO, "load_store: truncated file " + path);
     }
     cudaStream_t q = c->stream;
@@ -1369,6 +1596,34 @@ std::unique_ptr<prc_gpu_store> import_pstr(prc_gpu_ctx* c, const std::string& pa
     CK(launch_prep_ref(s.n_species, V, src, st->br_tot64.p, st->sp_ref.p, st->br_tot.p, nullptr, q,
                        &c->launches));
     c->sync();
+    if (materialize) {
+        std::vector<unsigned long long> rec(n);
+        for (unsigned long long k = 0; k < n; ++k) rec[k] = k;
+        up(st->m_rec, rec);
+        up(st->m_vbase, mh.vbase);
+        up(st->m_sbase, mh.sbase);
+        up(st->m_ebase, mh.ebase);
+        up(st->m_lbase, mh.lbase);
+        up(st->m_vmeta, mh.vmeta);
+        up(st->m_vvox, mh.vvox);
+        up(st->m_vct, mh.vct);
+        up(st->m_vsb, mh.vsb);
+        up(st->m_vse, mh.vse);
+        up(st->m_svox, mh.svox);
+        up(st->m_slen, mh.slen);
+        up(st->m_evert, mh.evert);
+        up(st->m_edet, mh.edet);
+        up(st->m_epix, mh.epix);
+        up(st->m_ecos, mh.ecos);
+        up(st->m_egeom, mh.egeom);
+        up(st->m_esb, mh.esb);
+        up(st->m_ese, mh.ese);
+        up(st->m_lvox, mh.lvox);
+        up(st->m_llen, mh.llen);
+        st->m_events = mh.evert.size();
+        st->m_eval.alloc(std::max<size_t>(mh.evert.size(), 1));
+        mat_ref_tables(c, st.get());
+    }
     return st;
 }
 
@@ -1417,9 +1672,19 @@ PRC_EXPORT int prc_gpu_nccl_unique_id(void* out128) {
     ABI_CATCH
 }
 
+PRC_EXPORT int prc_gpu_shard_range(uint64_t n, int rank, int world, uint64_t* lo, uint64_t* hi) {
+    if (!lo || !hi) return fail(PRC_ERR_INVALID, "prc_gpu_shard_range: null argument");
+    if (world < 1 || rank < 0 || rank >= world) return fail(PRC_ERR_INVALID, "rank/world out of range");
+    unsigned long long a, b;
+    shard_range(n, rank, world, &a, &b);
+    *lo = a;
+    *hi = b;
+    return PRC_OK;
+}
+
 PRC_EXPORT int prc_gpu_ctx_create_rank(int device, int rank, int world, const void* nccl_id,
                                        prc_gpu_ctx** out) {
-    if (!out || (world > 1 && !nccl_id)) return fail(PRC_ERR_INVALID, "prc_gpu_ctx_create_rank: null argument");
+    if (!out) return fail(PRC_ERR_INVALID, "prc_gpu_ctx_create_rank: null argument");
     if (world < 1 || rank < 0 || rank >= world) return fail(PRC_ERR_INVALID, "rank/world out of range");
     ABI_TRY
     auto c = std::make_unique<prc_gpu_ctx>();
@@ -1567,6 +1832,7 @@ PRC_EXPORT int prc_gpu_store_info_get(const prc_gpu_store* st, prc_gpu_store_inf
     o->sorted = st->sorted ? 1 : 0;
     o->max_size = st->max_B;
     o->device_bytes = st->device_bytes();
+    o->materialized = st->mat ? 1 : 0;
     return PRC_OK;
 }
 
@@ -1605,7 +1871,18 @@ PRC_EXPORT int prc_gpu_store_import_pstr(prc_gpu_ctx* ctx, const char* path, prc
     ABI_TRY
     begin(ctx);
     ctx->check_scene();
-    *out = import_pstr(ctx, path).release();
+    *out = import_pstr(ctx, path, false).release();
+    ++ctx->fwd_gen;
+    ABI_CATCH
+}
+
+PRC_EXPORT int prc_gpu_store_import_pstr_ex(prc_gpu_ctx* ctx, const char* path, int flags, prc_gpu_store** out) {
+    if (!ctx || !path || !out) return fail(PRC_ERR_INVALID, "prc_gpu_store_import_pstr_ex: null argument");
+    if (flags & ~PRC_IMPORT_MATERIALIZE) return fail(PRC_ERR_CONFIG, "prc_gpu_store_import_pstr_ex: unknown flags");
+    ABI_TRY
+    begin(ctx);
+    ctx->check_scene();
+    *out = import_pstr(ctx, path, (flags & PRC_IMPORT_MATERIALIZE) != 0).release();
     ++ctx->fwd_gen;
     ABI_CATCH
 }

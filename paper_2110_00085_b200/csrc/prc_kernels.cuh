@@ -227,3 +227,52 @@ cudaError_t launch_stats(const DScene& sc, const StoreView& st, unsigned long lo
 cudaError_t launch_events(const DScene& sc, const StoreView& st, int32_t* pix, double* cos_le,
                           double* geom, double* ray_w, cudaStream_t s,
                           unsigned long long* launches);
+
+// ---- materialized evaluation of imported PSTR stores (prc_materialized.cu) ----------
+// The reference's own path records as loaded by load_store (pathstore.cpp:455-516):
+// stored segment spans, events and LE spans, evaluated exactly as eval_record
+// (pathstore.cpp:115-238) reads them, in fp64.  Record arrays are in file order; the
+// storage position p of the (possibly sorted) store holds record rec[p].
+struct MatView {
+    unsigned long long n;                 // paths in this shard
+    const unsigned long long* rec;        // [n] record index of storage position p
+    const unsigned long long* v_base;     // [n_rec + 1] first vertex of record r
+    const unsigned long long* s_base;     // [n_rec] first segment span of record r
+    const unsigned long long* e_base;     // [n_rec + 1] first event of record r
+    const unsigned long long* l_base;     // [n_rec] first LE span of record r
+    const uint32_t* v_meta;               // kind | species << 8 | surface << 16
+    const int32_t* v_vox;
+    const double* v_ct;                   // cos_theta
+    const uint32_t *v_sb, *v_se;          // span range, relative to s_base[r]
+    const uint32_t* s_vox;
+    const double* s_len;
+    const uint32_t* e_vert;               // vertex b of the event
+    const int32_t* e_det;
+    const int32_t* e_pix;
+    const double *e_cos, *e_geom;
+    const uint32_t *e_sb, *e_se;          // LE span range, relative to l_base[r]
+    const uint32_t* l_vox;
+    const double* l_len;
+    double* e_val;                        // [events] forward value (K4 -> K5; wbuf / weight)
+};
+
+// Per-voxel fp64 context of make_context (pathstore.cpp:54-81): beta_t_tot, beta_ref_tot
+// and dbeta from the evaluated species values src_t and the store's reference values
+// ref (n_species x V, fp64).
+struct MatCtx {
+    const double* t[PRC_MAX_SPECIES];
+    const double* ref;     // n_species x V
+    double* bt_tot;        // V
+    double* br_tot;        // V
+    double* dbeta;         // V
+};
+cudaError_t launch_mat_prep(int n_species, long long V, const MatCtx& m, cudaStream_t s,
+                            unsigned long long* launches);
+// Forward (pathstore.cpp:115-185) or reverse (pathstore.cpp:187-238) over every path.
+cudaError_t launch_mat_forward(const DScene& sc, const MatView& mv, const MatCtx& m, const EvalArgs& ea,
+                               cudaStream_t s, unsigned long long* launches);
+cudaError_t launch_mat_gradient(const DScene& sc, const MatView& mv, const MatCtx& m, const EvalArgs& ea,
+                                cudaStream_t s, unsigned long long* launches);
+// dst[i] = src[perm[i]]
+cudaError_t launch_gather_u64(const uint32_t* perm, long long n, const unsigned long long* src,
+                              unsigned long long* dst, cudaStream_t s, unsigned long long* launches);

@@ -84,6 +84,7 @@ def load_library(path: Optional[str] = None):
         "prc_gpu_ctx_create": [C.c_int, C.POINTER(vp)],
         "prc_gpu_nccl_unique_id": [vp],
         "prc_gpu_ctx_create_rank": [C.c_int, C.c_int, C.c_int, vp, C.POINTER(vp)],
+        "prc_gpu_shard_range": [C.c_uint64, C.c_int, C.c_int, _u64p, _u64p],
         "prc_gpu_ctx_destroy": [vp],
         "prc_gpu_ctx_rank": [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)],
         "prc_gpu_ctx_set_option": [vp, C.c_char_p, C.c_int64],
@@ -97,6 +98,7 @@ def load_library(path: Optional[str] = None):
         "prc_gpu_store_sizes": [vp, _u32p],
         "prc_gpu_store_export_pstr": [vp, vp, C.c_char_p],
         "prc_gpu_store_import_pstr": [vp, C.c_char_p, C.POINTER(vp)],
+        "prc_gpu_store_import_pstr_ex": [vp, C.c_char_p, C.c_int, C.POINTER(vp)],
         "prc_gpu_store_set_generation": [vp, C.c_uint64],
         "prc_gpu_store_free": [vp],
         "prc_gpu_evaluate": [vp, vp, vp, C.POINTER(abi.EvalOpts), C.POINTER(abi.EvalResult)],
@@ -252,12 +254,20 @@ class Context:
         p = C.c_void_p()
         if world == 1 and nccl_id is None:
             _check(_lib.prc_gpu_ctx_create(device, C.byref(p)))
-        else:
-            buf = C.create_string_buffer(bytes(nccl_id), 128)
+        else:  # nccl_id None with world > 1: a detached shard (partial sums, no communicator)
+            buf = None if nccl_id is None else C.create_string_buffer(bytes(nccl_id), 128)
             _check(_lib.prc_gpu_ctx_create_rank(device, rank, world, buf, C.byref(p)))
         self.ptr = p.value
         self.scene: Optional[Scene] = None
         self.rank, self.world = rank, world
+
+    @staticmethod
+    def shard_range(n: int, rank: int, world: int):
+        """[lo, hi) of the global stream ids rank `rank` owns (host-only)."""
+        load_library()
+        lo, hi = C.c_uint64(), C.c_uint64()
+        _check(_lib.prc_gpu_shard_range(n, rank, world, C.byref(lo), C.byref(hi)))
+        return int(lo.value), int(hi.value)
 
     @staticmethod
     def nccl_unique_id() -> bytes:
@@ -312,9 +322,15 @@ class Context:
     def sort_by_size(self, store: PathStore):
         _check(_lib.prc_gpu_sort_by_size(self.ptr, store.ptr))
 
-    def load_store(self, path: str) -> PathStore:
+    def load_store(self, path: str, materialized: bool = False) -> PathStore:
+        """load_store (pathstore.cpp:455-516).  materialized=True evaluates the file's own
+        stored spans (PRC_IMPORT_MATERIALIZE); otherwise spans are recomputed on the device."""
         st = C.c_void_p()
-        _check(_lib.prc_gpu_store_import_pstr(self.ptr, path.encode(), C.byref(st)))
+        if materialized:
+            _check(_lib.prc_gpu_store_import_pstr_ex(self.ptr, path.encode(), abi.PRC_IMPORT_MATERIALIZE,
+                                                     C.byref(st)))
+        else:
+            _check(_lib.prc_gpu_store_import_pstr(self.ptr, path.encode(), C.byref(st)))
         return PathStore(self, st.value)
 
     # ------------------------------------------------------------------ K3-K5

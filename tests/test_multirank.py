@@ -25,7 +25,11 @@ def _free_port():
 
 
 def shard(n, rank, world):
-    return n * rank // world, n * (rank + 1) // world
+    """The engine's own partition (prc_gpu_shard_range, host-only: no device needed)."""
+    from paper_2110_00085_b200.gpu import Context
+    lo, hi = Context.shard_range(n, rank, world)
+    assert (lo, hi) == (n * rank // world, n * (rank + 1) // world)
+    return lo, hi
 
 
 def _worker(rank, world, port, pstr, name, out):
