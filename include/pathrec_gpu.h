@@ -290,6 +290,10 @@ int prc_gpu_opt_init(prc_gpu_ctx* ctx, const prc_gpu_params* initial, const doub
                      const prc_gpu_adam_config* adam);
 /* One recycled iteration over `store`; loss_out receives 0.5*||F - gt||^2. */
 int prc_gpu_opt_step(prc_gpu_ctx* ctx, const prc_gpu_store* store, double* loss_out);
+/* adam_step (inverse.cpp:41-67) with a caller-given gradient over the flattened unknowns
+ * (tomography: V values; reflectometry: dkappa_s, dgamma): one K6 update of the device-
+ * resident state, bit-identical to the reference's.  n must equal the unknown count. */
+int prc_gpu_opt_adam_step(prc_gpu_ctx* ctx, const double* grad, uint64_t n);
 /* Copies the current unknowns out (beta: V doubles or NULL). */
 int prc_gpu_opt_params(prc_gpu_ctx* ctx, double* beta_out, double* kappa_s, double* gamma);
 /* Current device forward images (pixel_count doubles) of the last step. */

@@ -212,6 +212,12 @@ class Reference:
         L.ref_render_json.argtypes = [C.c_char_p, C.c_uint64, C.c_uint64, _dp, C.c_uint64]
         L.ref_save_pfm.argtypes = [C.c_char_p, C.c_int, C.c_int, _dp]
         L.ref_load_pfm.argtypes = [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int), _dp, C.c_uint64]
+        L.ref_adam.argtypes = [C.c_uint64, _dp, _dp, C.c_int, C.c_double, C.c_double, C.c_double,
+                               C.c_double, C.c_int, _dp, C.c_int, C.c_int, _dp]
+        L.ref_loss.argtypes = [C.c_void_p, _dp, _dp, _dp]
+        L.ref_reconstruct_schedule.argtypes = [C.c_void_p, C.c_void_p, _dp, C.c_double, C.c_uint64, C.c_int,
+                                               _i32p, _u64p, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int,
+                                               _dp, _i32p, _u64p, _u64p]
         L.ref_segment_lengths.argtypes = [C.c_void_p, C.c_char_p, _u64p, _u32p, _u32p, _dp]
 
     def _err(self):
@@ -279,6 +285,46 @@ class Reference:
             raise ValueError(self._err())
         return dict(images=img, grad=grad[:scene.voxel_count], grad_kappa=gk.value,
                     grad_gamma=gg.value, clamp_events=int(cl.value), mean_correction=mc.value)
+
+    def adam(self, x0, grads, alpha, eta1=0.9, eta2=0.999, eps=1e-8, nonneg=True, step_scale=None,
+             phong=False):
+        """adam_step (inverse.cpp:41-67) over the rows of grads; the unknowns after each step."""
+        x0 = np.ascontiguousarray(x0, dtype=np.float64)
+        grads = np.ascontiguousarray(grads, dtype=np.float64).reshape(-1, x0.size)
+        ss = None if step_scale is None else np.ascontiguousarray(step_scale, dtype=np.float64)
+        out = np.zeros_like(grads)
+        if self.lib.ref_adam(x0.size, _ptr(x0, _dp), _ptr(grads, _dp), grads.shape[0], alpha, eta1, eta2, eps,
+                             1 if nonneg else 0, _ptr(ss, _dp), 0 if ss is None else ss.size, 1 if phong else 0,
+                             _ptr(out, _dp)):
+            raise ValueError(self._err())
+        return out
+
+    def loss(self, scene: Scene, F, gt) -> float:
+        h = scene.desc()
+        F = np.ascontiguousarray(F, dtype=np.float64)
+        gt = np.ascontiguousarray(gt, dtype=np.float64)
+        out = C.c_double()
+        if self.lib.ref_loss(h.ptr, _ptr(F, _dp), _ptr(gt, _dp), C.byref(out)):
+            raise ValueError(self._err())
+        return out.value
+
+    def reconstruct_schedule(self, scene: Scene, initial: ParamSet, gt, alpha: float, seed: int, stages,
+                             recycle_period: int, max_iterations: int, window: int, rel: float,
+                             workers: int = 1) -> dict:
+        h = scene.desc()
+        ph = ParamsHolder(initial)
+        gt = np.ascontiguousarray(gt, dtype=np.float64)
+        rc = np.array([[r, c] for r, c, _ in stages], np.int32).reshape(-1)
+        ns = np.array([n for _, _, n in stages], np.uint64)
+        loss = np.zeros(max_iterations)
+        stage = np.zeros(max_iterations, np.int32)
+        phases, trunc = C.c_uint64(), C.c_uint64()
+        if self.lib.ref_reconstruct_schedule(h.ptr, ph.ptr, _ptr(gt, _dp), alpha, seed, len(stages),
+                                             _ptr(rc, _i32p), _ptr(ns, _u64p), recycle_period, max_iterations,
+                                             window, rel, workers, _ptr(loss, _dp), _ptr(stage, _i32p),
+                                             C.byref(phases), C.byref(trunc)):
+            raise ValueError(self._err())
+        return dict(loss=loss, stage=stage, sampling_phases=int(phases.value), truncated_paths=int(trunc.value))
 
     def segment_lengths(self, scene: Scene, pstr: str):
         """segment_lengths (pathstore.cpp:296-313) of every record: (counts per segment, voxels,

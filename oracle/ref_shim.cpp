@@ -387,6 +387,91 @@ int ref_reconstruct(const prc_scene_desc* d, const prc_gpu_params* initial, cons
     }
 }
 
+/* adam_step (inverse.cpp:41-67) applied `steps` times with the given gradients (steps x n,
+ * dense over the flattened unknowns).  phong: the unknowns are (kappa_s, gamma); else beta.
+ * x_hist: steps x n unknowns after each update. */
+int ref_adam(uint64_t n, const double* x0, const double* grads, int steps, double alpha, double eta1,
+             double eta2, double eps, int nonneg, const double* step_scale, int n_ss, int phong,
+             double* x_hist) {
+    try {
+        OptState st;
+        if (phong) {
+            st.params.kappa_s = x0[0];
+            st.params.gamma = x0[1];
+        } else {
+            st.params.beta.assign(x0, x0 + n);
+        }
+        AdamConfig cfg;
+        cfg.alpha = alpha;
+        cfg.eta1 = eta1;
+        cfg.eta2 = eta2;
+        cfg.eps_guard = eps;
+        cfg.project_nonneg = nonneg != 0;
+        for (int i = 0; i < n_ss; ++i) cfg.step_scale.push_back(step_scale[i]);
+        for (int k = 0; k < steps; ++k) {
+            SparseGradient g;
+            g.kind = phong ? SparseGradient::Kind::Phong : SparseGradient::Kind::Tomography;
+            for (uint64_t i = 0; i < n; ++i) g.add(static_cast<int>(i), grads[k * n + i]);
+            adam_step(st, g, cfg);
+            for (uint64_t i = 0; i < n; ++i)
+                x_hist[k * n + i] = phong ? (i == 0 ? st.params.kappa_s : st.params.gamma) : st.params.beta[i];
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+/* loss (inverse.cpp:11-23) of images F against gt (scene's detector layout). */
+int ref_loss(const prc_scene_desc* d, const double* F, const double* gt, double* out) {
+    try {
+        Scene s = make_scene(d);
+        *out = loss(images_from(s, F), images_from(s, gt));
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+/* reconstruct() with a stage schedule (inverse.cpp:154-263).  stages: n_stages x
+ * (rows, cols) in stage_rc and n_paths in stage_n.  Per iteration: loss and stage. */
+int ref_reconstruct_schedule(const prc_scene_desc* d, const prc_gpu_params* initial, const double* gt,
+                             double alpha, uint64_t seed, int n_stages, const int* stage_rc,
+                             const uint64_t* stage_n, int recycle_period, int max_iterations, int window,
+                             double rel, int workers, double* loss_hist, int* stage_hist, uint64_t* phases_out,
+                             uint64_t* truncated_out) {
+    try {
+        Scene s = make_scene(d);
+        ParamSet init = make_params(s, initial);
+        ImageSet g = images_from(s, gt);
+        ReconstructOptions ro;
+        ro.adam.alpha = alpha;
+        ro.schedule.recycle_period = recycle_period;
+        ro.schedule.max_iterations = max_iterations;
+        ro.schedule.saturation_window = window;
+        ro.schedule.saturation_rel_improvement = rel;
+        for (int k = 0; k < n_stages; ++k) {
+            Stage st;
+            st.rows = stage_rc[2 * k];
+            st.cols = stage_rc[2 * k + 1];
+            st.n_paths = stage_n[k];
+            ro.schedule.stages.push_back(st);
+        }
+        ro.seed = seed;
+        ro.workers = workers;
+        ReconstructResult r = reconstruct(s, g, init, ro);
+        for (size_t i = 0; i < r.history.size(); ++i) {
+            loss_hist[i] = r.history[i].loss;
+            stage_hist[i] = r.history[i].stage;
+        }
+        *phases_out = r.sampling_phases;
+        *truncated_out = r.truncated_paths;
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
 /* space_carve (inverse.cpp:69-101): mask (V bytes) and initial beta (V doubles). */
 int ref_space_carve(const prc_scene_desc* d, const double* gt, double thr, double fill, uint8_t* mask,
                     double* beta) {

@@ -15,12 +15,29 @@ SOURCES = ["prc_kernels.cu", "prc_wavefront.cu", "prc_materialized.cu", "prc_cap
 HEADERS = ["prc_device.cuh", "prc_kernels.cuh", "prc_eval.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
+
+def _nccl_dir() -> str:
+    """The NCCL that torch loads (the nvidia-nccl wheel, 2.28).  Linking the engine against
+    the same library matters: both bind the soname libnccl.so.2, so whichever loads first
+    serves the process, and torch's libtorch_cuda needs 2.28 symbols the system 2.27
+    lacks (ncclDevCommCreate)."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia.nccl")
+    if spec and spec.submodule_search_locations:
+        d = list(spec.submodule_search_locations)[0]
+        if os.path.exists(os.path.join(d, "lib", "libnccl.so.2")):
+            return d
+    return ""
+
+
+NCCL_DIR = _nccl_dir()
+
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "--fmad=false", "-std=c++17",
     "-Xcompiler", "-fPIC,-ffp-contract=off,-fvisibility=hidden,-O2",
     "-Xptxas", "-v",
-]
+] + (["-I", os.path.join(NCCL_DIR, "include")] if NCCL_DIR else [])
 
 
 def _stale() -> bool:
@@ -55,8 +72,12 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str = OUT
             with open(os.path.join(SRC, s.replace(".cu", ".ptxas.txt")), "w") as f:
                 f.write("".join(l for l in se.splitlines(True) if "Compile time" not in l))
     tmp = out + ".tmp"
-    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs,
-           "-lnccl", "-Xlinker", "-rpath,/usr/lib/x86_64-linux-gnu"]
+    if NCCL_DIR:
+        nccl = ["-L" + os.path.join(NCCL_DIR, "lib"), "-l:libnccl.so.2", "-Xlinker",
+                "-rpath," + os.path.join(NCCL_DIR, "lib")]
+    else:
+        nccl = ["-lnccl", "-Xlinker", "-rpath,/usr/lib/x86_64-linux-gnu"]
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs, *nccl]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

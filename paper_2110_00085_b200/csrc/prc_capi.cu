@@ -2018,6 +2018,18 @@ static void bind_trace_species(prc_gpu_ctx* c) {
                           &c->launches));
 }
 
+// adam_step (inverse.cpp:41-67) on the device-resident unknowns with gradient g (device,
+// opt_n values): the same operations in the same order, so the update is the reference's
+// bit for bit (bias corrections c1, c2 from std::pow on the host, as there).
+static void adam_update(prc_gpu_ctx* c, const double* g) {
+    ++c->opt_t;
+    const double c1 = 1.0 - std::pow(c->adam.eta1, (double)c->opt_t);
+    const double c2 = 1.0 - std::pow(c->adam.eta2, (double)c->opt_t);
+    CK(launch_adam(c->opt_x.p, c->opt_m1.p, c->opt_m2.p, g, c->opt_n, c->adam.alpha, c->adam.eta1,
+                   c->adam.eta2, c->adam.eps_guard, c1, c2, c->opt_step_scale.p, c->n_step_scale,
+                   c->opt_mode == 0 ? (c->adam.project_nonneg ? 0 : 2) : 1, c->stream, &c->launches));
+}
+
 static double opt_step(prc_gpu_ctx* c, prc_gpu_store* st) {
     const DScene& s = c->dsc;
     cudaStream_t q = c->stream;
@@ -2042,9 +2054,6 @@ static double opt_step(prc_gpu_ctx* c, prc_gpu_store* st) {
     ea.per_species = c->opt_per_species && s.has_medium ? 1 : 0;
     ea.do_beta = s.has_medium && (s.unknown >= 0 || ea.per_species) ? 1 : 0;
     run_gradient(c, st, ea);
-    ++c->opt_t;
-    const double c1 = 1.0 - std::pow(c->adam.eta1, (double)c->opt_t);
-    const double c2 = 1.0 - std::pow(c->adam.eta2, (double)c->opt_t);
     const double* g;
     if (c->opt_mode == 0) {
         // per-type mode (config (c)): grad_j = g_span + g_vert[j] for every species j;
@@ -2056,9 +2065,7 @@ static double opt_step(prc_gpu_ctx* c, prc_gpu_store* st) {
         CK(launch_scale(c->g_phong.p, 2, scale, q, &c->launches));
         g = c->g_phong.p;
     }
-    CK(launch_adam(c->opt_x.p, c->opt_m1.p, c->opt_m2.p, g, c->opt_n, c->adam.alpha, c->adam.eta1,
-                   c->adam.eta2, c->adam.eps_guard, c1, c2, c->opt_step_scale.p, c->n_step_scale,
-                   c->opt_mode == 0 ? (c->adam.project_nonneg ? 0 : 2) : 1, q, &c->launches));
+    adam_update(c, g);
     double loss = 0.0;
     CK(cudaMemcpyAsync(&loss, c->loss.p, 8, cudaMemcpyDeviceToHost, q));
     CK(cudaEventRecord(c->ev[5], q));
@@ -2088,6 +2095,20 @@ PRC_EXPORT int prc_gpu_opt_step(prc_gpu_ctx* ctx, const prc_gpu_store* store, do
     store_for_scene(ctx, const_cast<prc_gpu_store*>(store));
     const double l = opt_step(ctx, const_cast<prc_gpu_store*>(store));
     if (loss_out) *loss_out = l;
+    ABI_CATCH
+}
+
+PRC_EXPORT int prc_gpu_opt_adam_step(prc_gpu_ctx* ctx, const double* grad, uint64_t n) {
+    if (!ctx || !grad) return fail(PRC_ERR_INVALID, "prc_gpu_opt_adam_step: null argument");
+    if (!ctx->opt_ready) return fail(PRC_ERR_INVALID, "prc_gpu_opt_adam_step: optimizer not initialised");
+    if ((long long)n != ctx->opt_n) return fail(PRC_ERR_CONFIG, "prc_gpu_opt_adam_step: gradient size != unknowns");
+    ABI_TRY
+    begin(ctx);
+    DBuf<double> g;
+    g.alloc((size_t)n);
+    CK(cudaMemcpyAsync(g.p, grad, (size_t)n * 8, cudaMemcpyHostToDevice, ctx->stream));
+    adam_update(ctx, g.p);
+    ctx->sync();
     ABI_CATCH
 }
 

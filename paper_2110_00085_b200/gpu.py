@@ -105,6 +105,7 @@ def load_library(path: Optional[str] = None):
         "prc_gpu_opt_init": [vp, vp, _dp, C.POINTER(abi.AdamConfig)],
         "prc_gpu_opt_step": [vp, vp, _dp],
         "prc_gpu_opt_params": [vp, _dp, _dp, _dp],
+        "prc_gpu_opt_adam_step": [vp, _dp, C.c_uint64],
         "prc_gpu_opt_images": [vp, _dp],
         "prc_gpu_reconstruct": [vp, vp, _dp, C.POINTER(abi.AdamConfig),
                                 C.POINTER(abi.ReconstructOpts), _dp, _u64p],
@@ -394,6 +395,11 @@ class Context:
         k, g = C.c_double(), C.c_double()
         _check(_lib.prc_gpu_opt_params(self.ptr, _ptr(beta, _dp), C.byref(k), C.byref(g)))
         return ParamSet(beta[:s.voxel_count] if s.unknown_species() >= 0 else None, k.value, g.value)
+
+    def opt_adam_step(self, grad: np.ndarray):
+        """adam_step (inverse.cpp:41-67) with a given gradient over the flattened unknowns."""
+        g = np.ascontiguousarray(grad, dtype=np.float64).reshape(-1)
+        _check(_lib.prc_gpu_opt_adam_step(self.ptr, _ptr(g, _dp), g.size))
 
     def opt_images(self) -> np.ndarray:
         out = np.zeros(self.scene.pixel_count)

@@ -79,3 +79,15 @@ def test_header_compiles_as_c_and_cpp(tmp_path):
         f.write_text('#include "pathrec_gpu.h"\nint main(void){return PRC_OK;}\n')
         subprocess.check_call([comp, "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"), str(f),
                                "-o", str(tmp_path / f"h_{ext}")])
+
+
+def test_library_loads_before_torch():
+    """The engine and torch share the soname libnccl.so.2: the engine links the NCCL torch
+    ships (2.28), so loading it first must not break a later `import torch` (torch's
+    libtorch_cuda needs 2.28-only symbols)."""
+    import subprocess
+    import sys
+    code = ("import ctypes, sys; sys.path.insert(0, %r); "
+            "from paper_2110_00085_b200.build import OUT; ctypes.CDLL(OUT); import torch.distributed") % ROOT
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]

@@ -160,3 +160,89 @@ def test_reconstruct_schedule_rejects_bad_schedules(ctx):
         ctx.reconstruct_schedule(s, gt, None, stages=[], max_iterations=2)
     with pytest.raises(gpu.PrcConfigError):
         ctx.reconstruct_schedule(s, gt, None, stages=[(8, 8, 0)], max_iterations=2)
+
+
+# ---------------------------------------------------------------- a14: the optimizer itself
+@pytest.mark.gpu
+@pytest.mark.parametrize("nonneg", [True, False])
+def test_adam_step_bit_identical_to_reference(ctx, ref, nonneg):
+    """K6 (k_adam) against the reference's adam_step (inverse.cpp:41-67) over 7 updates
+    with the same gradients: per-unknown step_scale (shorter than the unknowns), the
+    non-negativity projection (gradients push some voxels below zero), zero gradients."""
+    from tests.fixtures import FIXTURES, golden, perturbed
+    scene = FIXTURES["tomo2"]["scene"]()
+    g = golden("tomo2")["pert_res_grad"]
+    x0 = perturbed(scene).beta
+    rng = np.random.default_rng(5)
+    grads = np.stack([g * s for s in (1.0, -3.0, 0.5, 40.0, 0.0, -1.0, 7.0)])
+    grads[:, ::17] = 0.0
+    grads[3] += rng.normal(size=g.size) * np.abs(g).max()
+    ss = np.linspace(0.5, 2.0, g.size // 2)
+    ctx.upload(scene)
+    ctx.opt_init(S.ParamSet(x0), np.zeros(scene.pixel_count), alpha=1.5, project_nonneg=nonneg, step_scale=ss)
+    want = ref.adam(x0, grads, 1.5, nonneg=nonneg, step_scale=ss)
+    assert (want < 0).any() != nonneg and (want == 0).any() == nonneg
+    for k in range(len(grads)):
+        ctx.opt_adam_step(grads[k])
+        got = ctx.opt_params().beta
+        assert np.array_equal(got.view(np.uint64), want[k].view(np.uint64)), k
+
+
+@pytest.mark.gpu
+def test_adam_step_phong_clamp_bit_identical_to_reference(ctx, ref):
+    """Reflectometry unknowns (kappa_s, gamma) with step_scale [2, 100] and gradients that
+    drive kappa_s past 1 and below 0 and gamma below 0: the reference clamps kappa_s to
+    [0, 1] and gamma to >= 0 after every update."""
+    from tests.fixtures import FIXTURES
+    scene = FIXTURES["phong"]["scene"]()
+    grads = np.array([[-5.0, -2.0], [-5.0, 3.0], [8.0, 1.0], [9.0, 1.0], [9.0, 4.0], [0.0, 0.0], [-1e-3, -50.0]])
+    x0 = np.array([0.8, 0.5])
+    ctx.upload(scene)
+    ctx.opt_init(S.ParamSet(None, x0[0], x0[1]), np.zeros(scene.pixel_count), alpha=0.3, step_scale=[2.0, 100.0])
+    want = ref.adam(x0, grads, 0.3, step_scale=[2.0, 100.0], phong=True)
+    assert want[:, 0].max() == 1.0 and want[:, 0].min() == 0.0 and want[:, 1].min() == 0.0 < want[-1, 1]
+    for k in range(len(grads)):
+        ctx.opt_adam_step(grads[k])
+        p = ctx.opt_params()
+        got = np.array([p.kappa_s, p.gamma])
+        assert np.array_equal(got.view(np.uint64), want[k].view(np.uint64)), (k, got, want[k])
+
+
+@pytest.mark.gpu
+def test_device_loss_matches_reference_loss(ctx, ref, golden_dir):
+    """The loss K6 reduces on the device (k_loss_residual) is the reference's loss()
+    (inverse.cpp:11-23) of the same images, up to summation order."""
+    from tests.fixtures import FIXTURES, golden, perturbed
+    scene = FIXTURES["cloud"]["scene"]()
+    ctx.upload(scene)
+    st = ctx.load_store(str(golden_dir / "cloud.pstr"))
+    gt = 0.8 * golden("cloud")["ref_none_images"]
+    ctx.opt_init(perturbed(scene), gt, alpha=1e-3)
+    for _ in range(3):
+        loss = ctx.opt_step(st)
+        F = ctx.opt_images()
+        assert abs(loss - ref.loss(scene, F, gt)) <= 1e-14 * loss
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("window,rel", [(0, 0.01), (3, 1e9), (2, -1e9)])
+def test_schedule_decisions_match_reference(ctx, ref, window, rel):
+    """Stage application and saturation (inverse.cpp:175-189, 249-258) decided exactly as
+    the reference decides them: a window of 0 saturates at the first check, a huge relative
+    threshold as soon as the window is full, a negative one never.  Stages change only at
+    resample boundaries; the per-iteration stage sequence and the sampling-phase count
+    equal the reference loop's on the same problem, and the losses track it."""
+    import os
+    s = S.cloud_scene(8, 16, 16)
+    ctx.upload(s)
+    gt = ctx.render(s, RenderOptions(n_paths=100_000, seed=611)).images
+    init = S.ParamSet(np.full(s.voxel_count, s.species[0].extinction.mean()))
+    stages = [(4, 4, 10_000), (8, 8, 10_000), (16, 16, 10_000)]
+    out = ctx.reconstruct_schedule(s, gt, init, stages=stages, seed=33, recycle_period=3, max_iterations=20,
+                                   alpha=0.3, saturation_window=window, saturation_rel_improvement=rel)
+    r = ref.reconstruct_schedule(s, init, gt, 0.3, 33, stages, 3, 20, window, rel, workers=os.cpu_count() or 1)
+    assert list(out["history"]["stage"]) == list(r["stage"])
+    assert out["sampling_phases"] == r["sampling_phases"]
+    lo, lr = out["history"]["loss"], r["loss"]
+    assert np.all(np.abs(lo - lr) <= 0.05 * lr + 1e-30), np.c_[lo, lr]
+    print(f"window {window} rel {rel:g}: stages {list(r['stage'])}")
