@@ -122,6 +122,10 @@ typedef struct {
     prc_light_desc light;
     int n_detectors;
     const prc_detector_desc* detectors;
+    /* Nonzero when Scene::finalize (scene.cpp:8-14, 69-75) already ran on the host: detector
+     * and sun directions are unit vectors and are used as given.  Zero (the default): the
+     * engine finalizes them itself, exactly once. */
+    int finalized;
 } prc_scene_desc;
 
 /* ParamSet (transport.hpp:63-67): the unknowns decoupled from the scene.
@@ -253,7 +257,9 @@ enum {
     PRC_EVAL_WANT_GRAD = 2,
     PRC_EVAL_LEGACY_SCORE = 4,  /* pathstore.cpp:98-101 */
     PRC_EVAL_SELF_NORMALIZE = 8,/* rejected: PRC_ERR_CONFIG (not on the recycling loop) */
-    PRC_EVAL_PER_SPECIES = 16   /* per-type gradients: grad_out holds n_species x V */
+    PRC_EVAL_PER_SPECIES = 16,  /* per-type gradients: grad_out holds n_species x V */
+    PRC_EVAL_DETERMINISTIC = 32 /* bit-reproducible images (exact fixed-point pixel sums,
+                                   two forward passes); prc_gpu_render always does this */
 };
 
 typedef struct {
@@ -323,6 +329,8 @@ typedef struct {              /* Stage (inverse.hpp:23-26) */
     uint64_t n_paths;
 } prc_gpu_stage;
 
+struct prc_gpu_iteration_log_s; /* prc_gpu_iteration_log, below */
+
 typedef struct {              /* Schedule (inverse.hpp:28-35) + ReconstructOptions (:66-76) */
     uint64_t seed;
     int max_bounces;          /* trace budget (RenderOptions::max_bounces, default 500) */
@@ -336,9 +344,13 @@ typedef struct {              /* Schedule (inverse.hpp:28-35) + ReconstructOptio
     const char* checkpoint_dir;         /* NULL or "" disables checkpoints; rank 0 writes */
     int length_unit;          /* VGRD unit tag of the checkpoints (LengthUnit) */
     const prc_gpu_params* truth;        /* optional ground-truth unknowns for eps/delta */
+    /* ReconstructOptions::on_iteration (inverse.hpp:75): called once per iteration after
+     * logging, before the checkpoint and the update; may be NULL. */
+    void (*on_iteration)(const struct prc_gpu_iteration_log_s* row, void* user);
+    void* user;
 } prc_gpu_schedule;
 
-typedef struct {              /* IterationLog (inverse.hpp:46-53) */
+typedef struct prc_gpu_iteration_log_s { /* IterationLog (inverse.hpp:46-53) */
     int iter;
     double time_s, loss, eps, delta;
     int stage;

@@ -15,6 +15,7 @@ PRC_EVAL_WANT_GRAD = 2
 PRC_EVAL_LEGACY_SCORE = 4
 PRC_EVAL_SELF_NORMALIZE = 8
 PRC_EVAL_PER_SPECIES = 16
+PRC_EVAL_DETERMINISTIC = 32
 PRC_IMPORT_MATERIALIZE = 1
 
 c_double_p = C.POINTER(C.c_double)
@@ -51,7 +52,7 @@ class SceneDesc(C.Structure):
                 ("grid_origin", Vec3), ("voxel_size", Vec3), ("n_species", C.c_int),
                 ("species", C.POINTER(SpeciesDesc)), ("n_surfaces", C.c_int),
                 ("surfaces", C.POINTER(SurfaceDesc)), ("light", LightDesc),
-                ("n_detectors", C.c_int), ("detectors", C.POINTER(DetectorDesc))]
+                ("n_detectors", C.c_int), ("detectors", C.POINTER(DetectorDesc)), ("finalized", C.c_int)]
 
 
 class Params(C.Structure):
@@ -102,7 +103,7 @@ class Schedule(C.Structure):  # prc_gpu_schedule (Schedule + ReconstructOptions,
                 ("max_iterations", C.c_int), ("stages", C.POINTER(Stage)), ("n_stages", C.c_int),
                 ("saturation_window", C.c_int), ("saturation_rel_improvement", C.c_double),
                 ("checkpoint_every", C.c_int), ("checkpoint_dir", C.c_char_p), ("length_unit", C.c_int),
-                ("truth", C.POINTER(Params))]
+                ("truth", C.POINTER(Params)), ("on_iteration", C.c_void_p), ("user", C.c_void_p)]
 
 
 class IterationLog(C.Structure):  # prc_gpu_iteration_log (IterationLog, inverse.hpp:46-53)

@@ -11,7 +11,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libpathrec_gpu.so")
-SOURCES = ["prc_kernels.cu", "prc_wavefront.cu", "prc_materialized.cu", "prc_capi.cu"]
+SOURCES = ["prc_kernels.cu", "prc_wavefront.cu", "prc_materialized.cu", "prc_capi.cu", "prc_host_api.cu"]
 HEADERS = ["prc_device.cuh", "prc_kernels.cuh", "prc_eval.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
@@ -46,6 +46,7 @@ def _stale() -> bool:
     t = os.path.getmtime(OUT)
     deps = [os.path.join(SRC, f) for f in SOURCES + HEADERS]
     deps.append(os.path.join(HERE, "..", "include", "pathrec_gpu.h"))
+    deps.append(os.path.join(HERE, "..", "include", "pathrec.h"))
     deps.append(os.path.abspath(__file__))
     return any(os.path.getmtime(d) > t for d in deps)
 
@@ -77,7 +78,8 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str = OUT
                 "-rpath," + os.path.join(NCCL_DIR, "lib")]
     else:
         nccl = ["-lnccl", "-Xlinker", "-rpath,/usr/lib/x86_64-linux-gnu"]
-    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs, *nccl]
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs, *nccl,
+           "-Xlinker", "-soname," + os.path.basename(out)]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

@@ -121,6 +121,7 @@ struct prc_gpu_ctx {
     DBuf<double> scene_sp;        // device copy
     std::vector<prc_surface_desc> surfaces;
     std::vector<prc_detector_desc> det_desc;  // as uploaded (stage schedules re-finalize)
+    bool det_finalized = false;               // prc_scene_desc::finalized of the upload
     double scene_kappa = 0.0, scene_gamma = 0.0;
     // evaluation scratch
     DBuf<float> sp_t, bt_tot, dbeta;
@@ -128,6 +129,7 @@ struct prc_gpu_ctx {
     DBuf<double> param_beta, species_t, trace_sp, images, weights, g_span, g_vert, g_out, phong,
         g_phong, loss;
     DBuf<unsigned long long> clamps, u64tmp_a, u64tmp_b, n_trunc;
+    DBuf<unsigned long long> img_max, img_fx, img_limbs;  // deterministic images (image_pass)
     DBuf<uint32_t> u32tmp;
     DBuf<int> err;
     void* cub_tmp = nullptr;
@@ -350,14 +352,16 @@ void begin(prc_gpu_ctx* c) { CK(cudaSetDevice(c->device)); }
 // ----------------------------------------------------------------------- scene upload
 // Detector::finalize (scene.cpp:8-14) for every detector, at the resolution of the
 // descriptor or rows[k] x cols[k] when given; assigns image offsets, returns n_pix.
-long long finalize_detectors(DScene& s, const prc_detector_desc* dd, int n, const int* rows, const int* cols) {
+long long finalize_detectors(DScene& s, const prc_detector_desc* dd, int n, const int* rows, const int* cols,
+                             bool finalized) {
     long long off = 0;
     for (int k = 0; k < n; ++k) {
         const prc_detector_desc& q = dd[k];
         const int nr = rows ? rows[k] : q.rows, nc = cols ? cols[k] : q.cols;
         if (nr <= 0 || nc <= 0) throw Err(PRC_ERR_CONFIG, "detector: non-positive pixel grid");
         DDet& t = s.det[k];
-        const H3 dir = hnormalized(h3(q.direction));
+        // a finalized scene (Scene::finalize ran on the host) carries the unit direction
+        const H3 dir = finalized ? h3(q.direction) : hnormalized(h3(q.direction));
         const H3 right = hnormalized(hcross(dir, h3(q.up)));
         const H3 up = hcross(right, dir);
         put3(t.pos, h3(q.position));
@@ -460,14 +464,15 @@ void upload_scene(prc_gpu_ctx* c, const prc_scene_desc* d) {
     s.light_kind = d->light.kind == PRC_LIGHT_SUN ? 0 : 1;
     put3(s.light_pos, h3(d->light.position));
     H3 ld = h3(d->light.direction);
-    if (s.light_kind == 0) ld = hnormalized(ld);  // Scene::finalize, scene.cpp:71-74
+    if (s.light_kind == 0 && !d->finalized) ld = hnormalized(ld);  // Scene::finalize, scene.cpp:71-74
     put3(s.light_dir, ld);
     s.radiance = d->light.radiance;
     // emission_prefactor, transport.cpp:347-351
     s.prefactor = s.light_kind == 1 ? PRC_FOUR_PI * s.radiance
                                     : (s.bmax[0] - s.bmin[0]) * (s.bmax[1] - s.bmin[1]) * s.radiance;
     s.n_det = d->n_detectors;
-    const long long off = finalize_detectors(s, d->detectors, d->n_detectors, nullptr, nullptr);
+    c->det_finalized = d->finalized != 0;
+    const long long off = finalize_detectors(s, d->detectors, d->n_detectors, nullptr, nullptr, c->det_finalized);
     s.n_pix = off;
     // Fixed-point event term of single-species scenes (DScene::c1_fast): the range of
     // log(albedo * f) over cos in [-1, 1], from the phase function's extremes.
@@ -681,7 +686,7 @@ unsigned long long params_key(const prc_gpu_ctx* c, const prc_gpu_params* p, con
                               int flags) {
     unsigned long long h = mix64(0x1234567ull, (unsigned long long)(uintptr_t)st);
     h = mix64(h, (unsigned long long)c->mode);
-    h = mix64(h, (unsigned long long)(flags & PRC_EVAL_NORMALIZE));
+    h = mix64(h, (unsigned long long)(flags & (PRC_EVAL_NORMALIZE | PRC_EVAL_DETERMINISTIC)));
     if (!p) return mix64(h, 0xabcdefull);
     double kg[2] = {p->kappa_s, p->gamma};
     h = hash_doubles(h, kg, 2);
@@ -696,6 +701,7 @@ unsigned long long params_key(const prc_gpu_ctx* c, const prc_gpu_params* p, con
 // ----------------------------------------------------------------------- K3 + K4 + K5
 struct EvalRun {
     bool want_grad = false, per_species = false, legacy = false, normalize = true;
+    bool deterministic = false;  // bit-reproducible image (two passes, image_pass)
     const double* weights = nullptr;  // device
 };
 
@@ -780,6 +786,53 @@ EvalArgs eval_args(prc_gpu_ctx* c, prc_gpu_store* st, const EvalRun& er, const d
     return ea;
 }
 
+// Runs the image-producing kernel `launch` and all-reduces the raw images.  Deterministic
+// runs take two passes: the first finds the largest contribution (EvalArgs::img_mode 1), the
+// second adds exact 128-bit fixed-point values with a quantum 2^-101 of it (img_mode 2), so
+// the image does not depend on the order of the atomic additions, nor on how paths are
+// spread over ranks (render() is bit-reproducible under any worker count in the reference,
+// transport.hpp:171-173).  Contributions below the quantum (< 2^-101 of the largest) are
+// dropped.
+template <class F>
+void image_pass(prc_gpu_ctx* c, EvalArgs& ea, const EvalRun& er, F&& launch) {
+    cudaStream_t q = c->stream;
+    if (!er.deterministic) {
+        ea.img_mode = 0;
+        launch(ea);
+        CK(cudaEventRecord(c->ev[2], q));
+        c->allreduce(c->images.p, (size_t)c->n_pix);
+        return;
+    }
+    const size_t n = (size_t)c->n_pix;
+    c->img_max.grow(1);
+    c->img_fx.grow(std::max<size_t>(2 * n, 1));
+    c->img_limbs.grow(std::max<size_t>(3 * n, 1));
+    CK(cudaMemsetAsync(c->img_max.p, 0, 8, q));
+    ea.img_mode = 1;
+    ea.img_max = c->img_max.p;
+    launch(ea);
+    if (c->comm) NK(ncclAllReduce(c->img_max.p, c->img_max.p, 1, ncclUint64, ncclMax, c->comm, q));
+    unsigned long long bits = 0;
+    CK(cudaMemcpyAsync(&bits, c->img_max.p, 8, cudaMemcpyDeviceToHost, q));
+    c->sync();
+    double vmax;
+    std::memcpy(&vmax, &bits, 8);
+    CK(cudaMemsetAsync(c->img_fx.p, 0, c->img_fx.bytes(), q));
+    CK(cudaMemsetAsync(c->clamps.p, 0, sizeof(unsigned long long), q));  // the first pass counted them
+    int e = 0;
+    std::frexp(vmax, &e);  // vmax < 2^e: every term of the second pass is below 2^101
+    ea.img_mode = 2;
+    ea.img_fx = c->img_fx.p;
+    ea.img_inv_quantum = std::ldexp(1.0, std::min(1023, 101 - e));
+    const double quantum = std::ldexp(1.0, std::max(-1074, e - 101));
+    if (vmax > 0.0) launch(ea);
+    CK(cudaEventRecord(c->ev[2], q));
+    CK(launch_fixed_to_limbs(c->img_fx.p, (long long)n, c->img_limbs.p, q, &c->launches));
+    if (c->comm) NK(ncclAllReduce(c->img_limbs.p, c->img_limbs.p, 3 * n, ncclUint64, ncclSum, c->comm, q));
+    CK(launch_limbs_to_images(c->img_limbs.p, (long long)n, quantum, c->images.p, q, &c->launches));
+    ea.img_mode = 0;
+}
+
 // K3 prep + K4 forward (+ image allreduce).  Raw pixel sums land in c->images.
 // Events [0]..[3] bracket prep / forward / allreduce.
 void run_forward(prc_gpu_ctx* c, prc_gpu_store* st, const Resolved& r, const EvalRun& er,
@@ -797,11 +850,6 @@ void run_forward(prc_gpu_ctx* c, prc_gpu_store* st, const Resolved& r, const Eva
         phong_dev = c->phong.p;
     }
     if (st->mat) {  // stored spans (prc_materialized.cu)
-        if (!phong_dev) {
-            const double ph[2] = {r.kappa, r.gamma};
-            CK(cudaMemcpyAsync(c->phong.p, ph, sizeof ph, cudaMemcpyHostToDevice, q));
-            phong_dev = c->phong.p;
-        }
         for (int j = 0; j < PRC_MAX_SPECIES; ++j) st->m_ctx.t[j] = r.src[j];
         st->m_ctx.ref = st->m_ref64.p;
         st->m_ctx.bt_tot = st->m_bt.p;
@@ -815,9 +863,9 @@ void run_forward(prc_gpu_ctx* c, prc_gpu_store* st, const Resolved& r, const Eva
         ea = eval_args(c, st, er, phong_dev);
         c->timed_sub = c->timed_grad = false;
         CK(cudaEventRecord(c->ev[1], q));
-        CK(launch_mat_forward(s, st->mat_view(), st->m_ctx, ea, q, &c->launches));
-        CK(cudaEventRecord(c->ev[2], q));
-        c->allreduce(c->images.p, (size_t)c->n_pix);
+        image_pass(c, ea, er, [&](const EvalArgs& a) {
+            CK(launch_mat_forward(s, st->mat_view(), st->m_ctx, a, q, &c->launches));
+        });
         c->allreduce_u64(c->clamps.p, 1);
         CK(cudaEventRecord(c->ev[3], q));
         return;
@@ -849,14 +897,14 @@ void run_forward(prc_gpu_ctx* c, prc_gpu_store* st, const Resolved& r, const Eva
     if (c->mode == 0) {
         CK(launch_prefix(s, st->view(), ea, st->lp.p, q, &c->launches));
         CK(cudaEventRecord(c->ev[6], q));
-        CK(launch_le_forward(s, vertex_table(st), ea, st->lp.p, q, &c->launches));
-        st->geo_key = c->geo_gen;  // K4b wrote the event geometry (stream-ordered for later launches)
+        image_pass(c, ea, er, [&](const EvalArgs& a) {
+            CK(launch_le_forward(s, vertex_table(st), a, st->lp.p, q, &c->launches));
+            st->geo_key = c->geo_gen;  // K4b wrote the event geometry (stream-ordered for later launches)
+        });
     } else {
         st->geo_key = 0;  // the per-path kernels reuse ev_pix in path layout
-        CK(launch_forward(s, st->view(), ea, q, &c->launches));
+        image_pass(c, ea, er, [&](const EvalArgs& a) { CK(launch_forward(s, st->view(), a, q, &c->launches)); });
     }
-    CK(cudaEventRecord(c->ev[2], q));
-    c->allreduce(c->images.p, (size_t)c->n_pix);
     c->allreduce_u64(c->clamps.p, 1);
     CK(cudaEventRecord(c->ev[3], q));
 }
@@ -1800,6 +1848,7 @@ PRC_EXPORT int prc_gpu_render(prc_gpu_ctx* ctx, const prc_gpu_render_opts* opts,
     rr.kappa = r.kappa;
     rr.gamma = r.gamma;
     EvalRun er;
+    er.deterministic = true;  // render() is bit-reproducible (transport.hpp:171-173)
     run_eval(ctx, st.get(), rr, er, nullptr);
     CK(launch_scale(ctx->images.p, ctx->n_pix, 1.0 / (double)opts->n_paths, ctx->stream, &ctx->launches));
     copy_out(ctx, images_out, ctx->images.p, (size_t)ctx->n_pix);
@@ -1917,6 +1966,7 @@ PRC_EXPORT int prc_gpu_evaluate(prc_gpu_ctx* ctx, const prc_gpu_store* store,
     er.want_grad = (flags & PRC_EVAL_WANT_GRAD) != 0;
     er.per_species = (flags & PRC_EVAL_PER_SPECIES) != 0;
     er.legacy = (flags & PRC_EVAL_LEGACY_SCORE) != 0;
+    er.deterministic = (flags & PRC_EVAL_DETERMINISTIC) != 0;
     const double scale = (flags & PRC_EVAL_NORMALIZE) && st->n_global ? 1.0 / (double)st->n_global : 1.0;
     const unsigned long long key = params_key(ctx, params, st, flags);
     const bool reuse = er.want_grad && ctx->last_fwd_store == st && ctx->last_fwd_gen == ctx->fwd_gen &&
@@ -2245,7 +2295,7 @@ static void save_csv_host(const std::vector<prc_gpu_iteration_log>& rows, const 
 // Re-finalizes every detector at rows[k] x cols[k] and resizes the pixel buffers.
 static void set_resolution(prc_gpu_ctx* c, const std::vector<int>& rows, const std::vector<int>& cols) {
     const long long n_pix = finalize_detectors(c->dsc, c->det_desc.data(), (int)c->det_desc.size(), rows.data(),
-                                               cols.data());
+                                               cols.data(), c->det_finalized);
     c->n_pix = n_pix;
     c->images.alloc((size_t)n_pix);
     c->weights.alloc((size_t)n_pix);
@@ -2365,6 +2415,7 @@ PRC_EXPORT int prc_gpu_reconstruct_schedule(prc_gpu_ctx* ctx, const prc_gpu_para
         if (!truth.empty()) metrics_host(x_host.data(), truth.data(), truth.size(), &row.eps, &row.delta);
         rows.push_back(row);
         if (history) history[t] = row;
+        if (sch->on_iteration) sch->on_iteration(&row, sch->user);  // ReconstructOptions::on_iteration
         if (ckpt && ctx->rank == 0 && (t + 1) % sch->checkpoint_every == 0) {  // replicas agree: rank 0 writes
             const std::string dir(sch->checkpoint_dir);
             if (ctx->opt_mode == 0 && ctx->dsc.has_medium)

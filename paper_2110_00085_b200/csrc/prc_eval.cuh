@@ -6,6 +6,26 @@
 
 namespace prc {
 
+// image[idx] += v for a contribution v >= 0 (EvalArgs::img_mode).  Mode 2 adds the 128-bit
+// fixed-point value floor(v / quantum) as (hi, lo) u64 words: the lo atomic returns the old
+// word, so every wrap-around carries into hi exactly once and the final pair is the exact
+// sum in any order of the additions.
+__device__ __forceinline__ void image_add(const EvalArgs& ea, long long idx, double v) {
+    if (ea.img_mode == 0) {
+        atomicAdd(ea.images + idx, v);
+    } else if (ea.img_mode == 1) {
+        atomicMax(ea.img_max, (unsigned long long)__double_as_longlong(v));  // v >= 0: bits order as values
+    } else {
+        const double x = v * ea.img_inv_quantum;  // a power of two: exact
+        const double h = floor(x * 0x1p-64);
+        const unsigned long long hi = (unsigned long long)h;
+        const unsigned long long lo = (unsigned long long)(x - h * 0x1p64);
+        unsigned long long* cell = ea.img_fx + 2 * idx;
+        const unsigned long long old = atomicAdd(cell, lo);
+        atomicAdd(cell + 1, hi + (old + lo < old ? 1ull : 0ull));
+    }
+}
+
 __device__ __forceinline__ double scat_num(const DScene& sc, const float* sp, int vox, double c) {
     double num = 0.0;  // scat_num_t, pathstore.cpp:84-88
     for (int j = 0; j < sc.n_species; ++j)

@@ -304,7 +304,7 @@ __global__ void __launch_bounds__(kTPB) k_forward(const __grid_constant__ DScene
                                     ++clamps;
                                 }
                                 const double v = exp(logval) * geom * sc.prefactor;
-                                atomicAdd(ea.images + D.img_off + pix, v);
+                                image_add(ea, D.img_off + pix, v);
                                 val = (float)v;
                             }
                         } else {
@@ -808,6 +808,38 @@ cudaError_t launch_scale(double* x, long long n, double scale, cudaStream_t s,
                          unsigned long long* launches) {
     if (n == 0) return cudaSuccess;
     k_scale<<<grid_for(n, 256), 256, 0, s>>>(x, n, scale);
+    LAUNCH_DONE();
+}
+
+namespace {
+__global__ void k_fx_limbs(const unsigned long long* __restrict__ fx, long long n, unsigned long long* __restrict__ l) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const unsigned long long lo = fx[2 * i], hi = fx[2 * i + 1];
+    const unsigned long long m = (1ull << 43) - 1;
+    l[3 * i] = lo & m;
+    l[3 * i + 1] = ((lo >> 43) | (hi << 21)) & m;
+    l[3 * i + 2] = hi >> 22;
+}
+__global__ void k_limbs_images(const unsigned long long* __restrict__ l, long long n, double quantum,
+                               double* __restrict__ img) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    img[i] = (((double)l[3 * i + 2] * 0x1p86 + (double)l[3 * i + 1] * 0x1p43) + (double)l[3 * i]) * quantum;
+}
+}  // namespace
+
+cudaError_t launch_fixed_to_limbs(const unsigned long long* fx, long long n, unsigned long long* limbs,
+                                  cudaStream_t s, unsigned long long* launches) {
+    if (n == 0) return cudaSuccess;
+    k_fx_limbs<<<grid_for(n, 256), 256, 0, s>>>(fx, n, limbs);
+    LAUNCH_DONE();
+}
+
+cudaError_t launch_limbs_to_images(const unsigned long long* limbs, long long n, double quantum, double* images,
+                                   cudaStream_t s, unsigned long long* launches) {
+    if (n == 0) return cudaSuccess;
+    k_limbs_images<<<grid_for(n, 256), 256, 0, s>>>(limbs, n, quantum, images);
     LAUNCH_DONE();
 }
 

@@ -87,6 +87,15 @@ struct EvalArgs {
     long long g_pad_stride;
     int g_pad_copies;
     int per_species, legacy, do_beta;
+    // Image accumulation (image_add, prc_eval.cuh): 0 fp64 reductions into `images`
+    // (default); 1 the largest contribution's bits into *img_max (first pass of a
+    // deterministic evaluation); 2 exact 128-bit fixed-point sums into img_fx (two u64 per
+    // pixel, quantum 1 / img_inv_quantum), independent of the order of the additions, so the
+    // image is bit-reproducible (render() is, transport.hpp:171-173).
+    int img_mode;
+    unsigned long long* img_max;
+    unsigned long long* img_fx;
+    double img_inv_quantum;
 };
 
 struct TraceArgs {
@@ -123,6 +132,13 @@ cudaError_t launch_gradient(const DScene& sc, const StoreView& st, const EvalArg
                             cudaStream_t s, unsigned long long* launches);
 cudaError_t launch_scale(double* x, long long n, double scale, cudaStream_t s,
                          unsigned long long* launches);
+// Deterministic images (EvalArgs::img_mode 2): the 128-bit sums (hi, lo) split into three
+// 43-bit limbs (so ranks can add them with an integer allreduce without losing carries),
+// then images[p] = ((l2 * 2^86 + l1 * 2^43) + l0) * quantum.
+cudaError_t launch_fixed_to_limbs(const unsigned long long* fx, long long n, unsigned long long* limbs,
+                                  cudaStream_t s, unsigned long long* launches);
+cudaError_t launch_limbs_to_images(const unsigned long long* limbs, long long n, double quantum, double* images,
+                                   cudaStream_t s, unsigned long long* launches);
 cudaError_t launch_combine_grad(const double* g_span, const double* g_vert, int n_out, long long V,
                                 double scale, double* out, cudaStream_t s,
                                 unsigned long long* launches);

@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(kFwdTPB, kFwdMinBlocks) k_le_forward(const __g
         if (SC && direct != 0.0) {
             const double contrib = direct * geom * sc.prefactor;
             val = (float)contrib;
-            if (contrib != 0.0) atomicAdd(ea.images + sc.det[k].img_off + pix, contrib);
+            if (contrib != 0.0) image_add(ea, sc.det[k].img_off + pix, contrib);
         } else if (logval != -INFINITY) {
             if (sc.has_medium) {
                 logval -= sc.pad_walk ? dda_optical_depth_pad(sc, x, w, r, ea.bt_pad)
@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(kFwdTPB, kFwdMinBlocks) k_le_forward(const __g
             }
             const double contrib = exp(logval) * geom * sc.prefactor;
             val = (float)contrib;
-            if (contrib != 0.0) atomicAdd(ea.images + sc.det[k].img_off + pix, contrib);
+            if (contrib != 0.0) image_add(ea, sc.det[k].img_off + pix, contrib);
         }
         if (act) {
             vt.ev_val[e] = val;

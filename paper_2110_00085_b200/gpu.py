@@ -166,6 +166,7 @@ class EvalOptions:
     self_normalize: bool = False
     pixel_weights: Optional[np.ndarray] = None
     per_species: bool = False
+    deterministic: bool = False  # bit-reproducible images (PRC_EVAL_DETERMINISTIC)
 
     def flags(self) -> int:
         f = 0
@@ -179,6 +180,8 @@ class EvalOptions:
             f |= abi.PRC_EVAL_SELF_NORMALIZE
         if self.per_species:
             f |= abi.PRC_EVAL_PER_SPECIES
+        if self.deterministic:
+            f |= abi.PRC_EVAL_DETERMINISTIC
         return f
 
 

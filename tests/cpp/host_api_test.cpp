@@ -13,10 +13,9 @@ using namespace pathrec_gpu;
 
 static Scene two_species_cube(int n) {  // tests/helpers.hpp:56-79
     Scene s;
-    s.bounds_min = {0, 0, 0};
-    s.bounds_max = {1, 1, 1};
+    s.bounds = {{0, 0, 0}, {1, 1, 1}};
     GridGeometry g;
-    g.dims[0] = g.dims[1] = g.dims[2] = n;
+    g.dims = {n, n, n};
     g.voxel_size = {1.0 / n, 1.0 / n, 1.0 / n};
     ParticleSpecies cloud, air;
     cloud.extinction.geom = air.extinction.geom = g;
@@ -51,7 +50,7 @@ int main() {
     ro.keep_paths = true;
     RenderResult rr = render(ctx, s, ro);
     sort_by_size(*rr.store);
-    if (!rr.store->sorted_flag()) return 2;
+    if (!rr.store->sorted_flag) return 2;
     ParamSet t = params_from_scene(s);
     for (size_t v = 0; v < t.beta.size(); ++v) t.beta[v] *= 1.0 + 0.02 * (v % 7);
     ImageSet w = rr.images;
@@ -100,32 +99,32 @@ int main() {
         threw = true;
     }
     if (!threw) return 7;
-    // Algorithm 2 on the device
+    // Algorithm 2 on the device: one stage, resample every 5 iterations
     ImageSet gt = render(ctx, s, RenderOptions{20000, 99, 1, 500, -1, false}).images;
     ReconstructOptions opt;
     opt.adam.alpha = 0.05;
-    opt.recycle_period = 5;
-    opt.max_iterations = 12;
-    opt.n_paths = 5000;
+    opt.schedule.recycle_period = 5;
+    opt.schedule.max_iterations = 12;
+    opt.schedule.stages = {Stage{0, 0, 5000}};
     ParamSet init;
     init.beta.assign(64, 3.0);
     ReconstructResult res = reconstruct(ctx, s, gt, init, opt);
     std::printf("reconstruct: phases %llu loss %.3e -> %.3e\n", (unsigned long long)res.sampling_phases,
-                res.loss.front(), res.loss.back());
+                res.history.front().loss, res.history.back().loss);
     // phases = ceil(T / N_r) (acceptance.cpp:470); finite losses; the iterate moved
     bool finite = true, moved = false;
-    for (double l : res.loss) finite = finite && std::isfinite(l);
+    for (const auto& h : res.history) finite = finite && std::isfinite(h.loss);
     for (double b : res.params.beta) moved = moved || b != 3.0;
     if (res.sampling_phases != 3 || !finite || !moved) return 8;
     // the stage-scheduled loop: a coarse 4x4 stage, then the uploaded resolution
-    ScheduleOptions so;
+    ReconstructOptions so;
     so.adam.alpha = 0.05;
     so.schedule.recycle_period = 4;
     so.schedule.max_iterations = 12;
     so.schedule.saturation_window = 3;
     so.schedule.saturation_rel_improvement = 1.0;  // saturate as soon as the window is full
     so.schedule.stages = {Stage{4, 4, 5000}, Stage{0, 0, 5000}};
-    ScheduleResult sr = reconstruct(ctx, s, gt, init, so);
+    ReconstructResult sr = reconstruct(ctx, s, gt, init, so);
     std::printf("schedule: phases %llu stages %d..%d\n", (unsigned long long)sr.sampling_phases,
                 sr.history.front().stage, sr.history.back().stage);
     if (sr.sampling_phases != 3 || sr.history.size() != 12 || sr.history[3].stage != 0 || sr.history[4].stage != 1)

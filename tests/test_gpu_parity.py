@@ -732,3 +732,22 @@ def test_import_range_checks_voxel_ids(ctx, golden_dir, tmp_path):
     bad.write_bytes(bytes(raw))
     with pytest.raises(PrcIOError, match="voxel"):
         ctx.load_store(str(bad))
+
+
+def test_render_is_bit_reproducible(ctx):
+    """render() is bit-reproducible for fixed (seed, n_paths) (transport.hpp:171-173): the
+    fresh image is summed in exact 128-bit fixed point, so the order of the device atomics
+    does not matter.  The deterministic recycled evaluation agrees with the fp64-atomic one
+    to rounding, and is itself reproducible."""
+    s = S.cloud_scene(16, 12, 12)
+    ctx.upload(s)
+    a = ctx.render(s, RenderOptions(n_paths=200_000, seed=5, keep_paths=True))
+    b = ctx.render(s, RenderOptions(n_paths=200_000, seed=5))
+    assert np.array_equal(a.images.view(np.uint64), b.images.view(np.uint64))
+    t = perturbed(s)
+    d1 = ctx.evaluate_store(s, a.store, t, EvalOptions(deterministic=True)).images
+    d2 = ctx.evaluate_store(s, a.store, t, EvalOptions(deterministic=True)).images
+    f = ctx.evaluate_store(s, a.store, t, EvalOptions()).images
+    assert np.array_equal(d1.view(np.uint64), d2.view(np.uint64))
+    assert img_err(d1, f) <= 1e-13
+    assert img_err(ctx.recycled_render(s, a.store, None), a.images) <= 1e-13

@@ -14,7 +14,7 @@ def build_host_test(tmp_path):
     port = build_port()
     exe = str(tmp_path / "host_api_test")
     subprocess.check_call([
-        "g++", "-std=c++17", "-O2", "-Wall", "-I", os.path.join(ROOT, "include"),
+        "g++", "-std=c++20", "-O2", "-Wall", "-I", os.path.join(ROOT, "include"),
         os.path.join(ROOT, "tests", "cpp", "host_api_test.cpp"), "-o", exe,
         lib, port, f"-Wl,-rpath,{os.path.dirname(lib)}:{os.path.dirname(port)}"])
     return exe
