@@ -189,9 +189,21 @@ def run_ours(args):
     if args.grad_copies is not None:
         ctx.set_option("grad_copies", args.grad_copies)
     ctx.upload(scene)
+    tp = t_params(scene)
+    # warm-up resample on a small store: loads every kernel module (CUDA lazy loading) and
+    # sizes the context's scratch, so the timed resample below is a steady-state one
+    warm = ctx.render(scene, RenderOptions(n_paths=min(n_paths, 50_000), seed=1, keep_paths=True,
+                                           max_bounces=max_bounces(cfg), images=False)).store
+    ctx.sort_by_size(warm)
+    ctx.opt_init(tp, np.zeros(scene.pixel_count), alpha=1e-3)
+    ctx.opt_step(warm)
+    warm.free()
+    # the resample phase of the loop (inverse.cpp:175-204): trace (K1) + sort (K2); the
+    # resample iteration's forward is the recycled one at the sampling point
+    barrier(pg)
     t0 = time.time()
     rr = ctx.render(scene, RenderOptions(n_paths=n_paths, seed=7, keep_paths=True,
-                                         max_bounces=max_bounces(cfg)))
+                                         max_bounces=max_bounces(cfg), images=False))
     t1 = time.time()
     store = rr.store
     if not args.no_sort:
@@ -201,10 +213,14 @@ def run_ours(args):
     stats = ctx.store_stats(store)  # global (allreduced)
     seg_global = reduce_sum(pg, info["segments"])
     vert_global = reduce_sum(pg, info["vertices"])
-    gt = 0.9 * rr.images  # synthetic measurement (residual = F_t - 0.9 F_ref)
-    tp = t_params(scene)
-    ctx.opt_init(tp, gt, alpha=1e-3 if cfg != "d" else 1e-3)
-    for _ in range(args.warmup):
+    gt = 0.9 * ctx.recycled_render(scene, store, None)  # synthetic measurement: residual = F_t - 0.9 F_ref
+    ctx.opt_init(tp, gt, alpha=1e-3)
+    # the first iteration over a fresh store also builds the Morton vertex table and the
+    # event-geometry cache: its extra time is charged to the resample phase
+    ctx.timer_start()
+    ctx.opt_step(store)
+    first_ms = reduce_max(pg, ctx.timer_stop())
+    for _ in range(max(0, args.warmup - 1)):
         ctx.opt_step(store)
     # ---- timed region: exactly K recycled iterations
     barrier(pg)
@@ -290,9 +306,12 @@ def run_ours(args):
                        "segments": int(seg_global), "vertices": int(vert_global),
                        "events": int(E), "live_span_incidences": int(W_live),
                        "l2": "store >> L2 (126 MB), no flush needed",
-                       "trace_s": round(trace_s, 3), "sort_s": round(sort_s, 3),
+                       "trace_s": round(trace_s, 4), "sort_s": round(sort_s, 4),
+                       "first_iteration_ms": round(first_ms, 3),
                        "recycle_period": RECYCLE_PERIOD,
-                       "amortized_seg_per_s": seg_global / (ms_per_step / 1e3 + (trace_s + sort_s) / RECYCLE_PERIOD),
+                       "amortized_seg_per_s": seg_global / (
+                           ms_per_step / 1e3 + (trace_s + sort_s + max(0.0, first_ms - ms_per_step) / 1e3)
+                           / RECYCLE_PERIOD),
                        "sorted_by_B": not args.no_sort,
                        "mode": "per_path" if args.mode == 1 else "wavefront",
                        "spread": args.spread, "packet": args.packet,

@@ -199,8 +199,9 @@ typedef struct {
 } prc_gpu_render_opts;
 
 /* Traces n_paths paths under `params` (NULL: scene values; bind_params semantics,
- * inverse.cpp:144-150) and evaluates them at that point (the fresh image).
- * images_out: host buffer of pixel_count doubles, normalised by 1/N (may be NULL).
+ * inverse.cpp:144-150) and evaluates them at that point (the fresh image, bit-reproducible
+ * for fixed seed and n_paths).  images_out: host buffer of pixel_count doubles, normalised
+ * by 1/N; NULL skips the fresh evaluation (trace only, as a resample of reconstruct).
  * store_out: non-NULL keeps the path store (keep_paths). */
 int prc_gpu_render(prc_gpu_ctx* ctx, const prc_gpu_render_opts* opts, const prc_gpu_params* params,
                    double* images_out, uint64_t* truncated_out, prc_gpu_store** store_out);

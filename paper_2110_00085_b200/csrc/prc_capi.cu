@@ -1842,6 +1842,12 @@ PRC_EXPORT int prc_gpu_render(prc_gpu_ctx* ctx, const prc_gpu_render_opts* opts,
                 CK(cudaMemcpyAsync(ctx->trace_sp.p + (size_t)j * ctx->V, r.src[j],
                                    (size_t)ctx->V * 8, cudaMemcpyDeviceToDevice, ctx->stream));
     auto st = trace_store(ctx, opts, ctx->trace_sp.p, r.kappa, r.gamma, nullptr, true);
+    if (!images_out) {  // nobody reads the fresh image: trace only (the resample of reconstruct)
+        ctx->sync();
+        if (truncated_out) *truncated_out = global_count(ctx, st->truncated);
+        if (store_out) *store_out = st.release();
+        return PRC_OK;
+    }
     // fresh evaluation at the sampling point (render's evaluate_store, transport.cpp:432-435)
     Resolved rr;
     for (int j = 0; j < s.n_species; ++j) rr.src[j] = ctx->trace_sp.p + (size_t)j * ctx->V;

@@ -154,6 +154,7 @@ class RenderOptions:
     max_bounces: int = 500
     max_scatter_events: int = -1
     keep_paths: bool = False
+    images: bool = True  # False: trace only, no fresh evaluation (images None)
 
 
 @dataclass
@@ -315,7 +316,7 @@ class Context:
         s = self._use(scene)
         o = abi.RenderOpts(opt.n_paths, opt.seed, opt.max_bounces, opt.max_scatter_events)
         ph = ParamsHolder(params)
-        img = np.zeros(s.pixel_count)
+        img = np.zeros(s.pixel_count) if opt.images else None
         tr = C.c_uint64()
         st = C.c_void_p()
         _check(_lib.prc_gpu_render(self.ptr, C.byref(o), ph.ptr, _ptr(img, _dp), C.byref(tr),
