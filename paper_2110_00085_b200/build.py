@@ -11,7 +11,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libpathrec_gpu.so")
-SOURCES = ["prc_kernels.cu", "prc_wavefront.cu", "prc_materialized.cu", "prc_capi.cu", "prc_host_api.cu"]
+SOURCES = ["prc_kernels.cu", "prc_wavefront.cu", "prc_materialized.cu", "prc_nvls.cu", "prc_capi.cu", "prc_host_api.cu"]
 HEADERS = ["prc_device.cuh", "prc_kernels.cuh", "prc_eval.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 

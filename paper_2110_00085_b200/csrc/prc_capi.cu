@@ -130,6 +130,11 @@ struct prc_gpu_ctx {
         g_phong, loss;
     DBuf<unsigned long long> clamps, u64tmp_a, u64tmp_b, n_trunc;
     DBuf<unsigned long long> img_max, img_fx, img_limbs;  // deterministic images (image_pass)
+    const double* grad_res = nullptr;  // combined, reduced gradient of the last run_gradient
+    // NVLS multicast reduction (option "nvls", prc_nvls.cu): [0, n_pix) images, then the
+    // n_species x V gradient
+    bool nvls_enable = false, nvls_emulate = false;
+    NvlsState* nvls = nullptr;
     DBuf<uint32_t> u32tmp;
     DBuf<int> err;
     void* cub_tmp = nullptr;
@@ -167,6 +172,7 @@ struct prc_gpu_ctx {
             if (e) cudaEventDestroy(e);
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
+        nvls_destroy(nvls);
         if (comm) ncclCommDestroy(comm);
         if (stream) cudaStreamDestroy(stream);
     }
@@ -379,6 +385,8 @@ long long finalize_detectors(DScene& s, const prc_detector_desc* dd, int n, cons
     return off;
 }
 
+void nvls_setup(prc_gpu_ctx* c);
+
 void upload_scene(prc_gpu_ctx* c, const prc_scene_desc* d) {
     ++c->scene_gen;
     ++c->geo_gen;  // cameras / species / surfaces may change: cached event geometry is stale
@@ -565,6 +573,24 @@ void upload_scene(prc_gpu_ctx* c, const prc_scene_desc* d) {
     c->err.alloc(1);
     c->have_scene = true;
     c->opt_ready = false;
+    nvls_setup(c);
+}
+
+// (Re)creates the NVLS multicast buffer for the current images and gradient sizes
+// (collective over the ranks when world > 1: every rank uploads the same scene).
+void nvls_setup(prc_gpu_ctx* c) {
+    const size_t need = (size_t)c->n_pix + (size_t)std::max(1, c->dsc.n_species) * (size_t)std::max<long long>(c->V, 1);
+    if (!c->nvls_enable) {
+        nvls_destroy(c->nvls);
+        c->nvls = nullptr;
+        return;
+    }
+    if (c->nvls && nvls_capacity(c->nvls) >= need) return;
+    nvls_destroy(c->nvls);
+    c->nvls = nullptr;
+    std::string err;
+    c->nvls = nvls_create(c->comm, c->comm ? c->world : 1, c->device, need, c->nvls_emulate, &err);
+    if (!c->nvls) throw Err(PRC_ERR_CUDA, "nvls: " + err);
 }
 
 // Species source pointers + Phong values for the evaluated parameters.
@@ -702,6 +728,7 @@ unsigned long long params_key(const prc_gpu_ctx* c, const prc_gpu_params* p, con
 struct EvalRun {
     bool want_grad = false, per_species = false, legacy = false, normalize = true;
     bool deterministic = false;  // bit-reproducible image (two passes, image_pass)
+    double grad_scale = 1.0;     // scale of the combined gradient (1 / N with normalize)
     const double* weights = nullptr;  // device
 };
 
@@ -800,7 +827,18 @@ void image_pass(prc_gpu_ctx* c, EvalArgs& ea, const EvalRun& er, F&& launch) {
         ea.img_mode = 0;
         launch(ea);
         CK(cudaEventRecord(c->ev[2], q));
-        c->allreduce(c->images.p, (size_t)c->n_pix);
+        if (c->nvls) {  // the images' cross-rank sum by multimem reductions (prc_nvls.cu)
+            NvlsFold a{};
+            a.g_span = c->images.p;
+            a.n_out = 1;
+            a.V = c->n_pix;
+            a.nx = a.ny = a.pnx = a.pnxny = 1;
+            a.scale = 1.0;
+            CK(nvls_fold(c->nvls, a, 0, q, &c->launches));
+            CK(cudaMemcpyAsync(c->images.p, nvls_local(c->nvls), (size_t)c->n_pix * 8, cudaMemcpyDeviceToDevice, q));
+        } else {
+            c->allreduce(c->images.p, (size_t)c->n_pix);
+        }
         return;
     }
     const size_t n = (size_t)c->n_pix;
@@ -909,8 +947,12 @@ void run_forward(prc_gpu_ctx* c, prc_gpu_store* st, const Resolved& r, const Eva
     CK(cudaEventRecord(c->ev[3], q));
 }
 
-// K5 gradient (+ gradient allreduce) with weights ea.weights.  Event [4] after K5.
-void run_gradient(prc_gpu_ctx* c, prc_gpu_store* st, const EvalArgs& ea) {
+// K5 gradient with weights ea.weights, then its reduction over ranks and the combination
+// grad_j = scale (g_span + g_vert[j]) (n_out species slices) into c->grad_res.  Event [4]
+// after K5.  With NVLS (option "nvls") one fold kernel does the padded-copy sum, the
+// combination and the cross-rank sum through multimem reductions (prc_nvls.cu); otherwise
+// k_unpad_add, ncclAllReduce of g_span and g_vert, and k_combine.
+void run_gradient(prc_gpu_ctx* c, prc_gpu_store* st, const EvalArgs& ea, int n_out, double scale) {
     const DScene& s = c->dsc;
     cudaStream_t q = c->stream;
     CK(cudaMemsetAsync(c->g_span.p, 0, c->g_span.bytes(), q));
@@ -927,13 +969,38 @@ void run_gradient(prc_gpu_ctx* c, prc_gpu_store* st, const EvalArgs& ea) {
         CK(cudaEventRecord(c->ev[7], q));
         c->timed_grad = true;
         CK(launch_path_gradient(s, st->view(), ea, st->own.p, q, &c->launches));
-        if (s.pad_walk) CK(launch_unpad_add(s, c->g_pad.p, c->g_pad_copies, ea.g_pad_stride, c->g_span.p, q, &c->launches));
     } else {
         CK(launch_gradient(s, st->view(), ea, q, &c->launches));
     }
+    const bool padded = !st->mat && c->mode == 0 && s.pad_walk;
     CK(cudaEventRecord(c->ev[4], q));
-    c->allreduce(c->g_span.p, c->g_span.n);
-    c->allreduce(c->g_vert.p, c->g_vert.n);
+    c->grad_res = nullptr;
+    if (ea.do_beta && c->nvls) {
+        NvlsFold a{};
+        if (padded) {
+            a.g_pad = c->g_pad.p;
+            a.copies = c->g_pad_copies;
+            a.stride = ea.g_pad_stride;
+        } else {
+            a.g_span = c->g_span.p;
+        }
+        a.g_vert = c->g_vert.p;
+        a.n_out = n_out;
+        a.V = c->V;
+        a.nx = s.dims[0];
+        a.ny = s.dims[1];
+        a.pnx = s.pnx;
+        a.pnxny = s.pnxny;
+        a.scale = scale;
+        CK(nvls_fold(c->nvls, a, (size_t)c->n_pix, q, &c->launches));
+        c->grad_res = nvls_local(c->nvls) + c->n_pix;
+    } else if (ea.do_beta) {
+        if (padded) CK(launch_unpad_add(s, c->g_pad.p, c->g_pad_copies, ea.g_pad_stride, c->g_span.p, q, &c->launches));
+        c->allreduce(c->g_span.p, c->g_span.n);
+        c->allreduce(c->g_vert.p, c->g_vert.n);
+        CK(launch_combine_grad(c->g_span.p, c->g_vert.p, n_out, c->V, scale, c->g_out.p, q, &c->launches));
+        c->grad_res = c->g_out.p;
+    }
     c->allreduce(c->g_phong.p, 2);
 }
 
@@ -945,7 +1012,7 @@ unsigned long long run_eval(prc_gpu_ctx* c, prc_gpu_store* st, const Resolved& r
     EvalArgs ea;
     run_forward(c, st, r, er, phong_dev, ea);
     if (er.want_grad)
-        run_gradient(c, st, ea);
+        run_gradient(c, st, ea, er.per_species ? c->dsc.n_species : 1, er.grad_scale);
     else
         CK(cudaEventRecord(c->ev[4], q));
     unsigned long long cl = 0;
@@ -1772,6 +1839,10 @@ PRC_EXPORT int prc_gpu_ctx_set_option(prc_gpu_ctx* ctx, const char* key, int64_t
     } else if (k == "grad_copies") {
         if (value < 0 || value > 64) return fail(PRC_ERR_CONFIG, "grad_copies must be in 0..64");
         ctx->grad_copies_max = (int)value;
+    } else if (k == "nvls") {  // applied at the next scene upload; 2: fold without multicast (1 rank)
+        if (value < 0 || value > 2) return fail(PRC_ERR_CONFIG, "nvls must be 0, 1 or 2");
+        ctx->nvls_enable = value != 0;
+        ctx->nvls_emulate = value == 2;
     } else if (k == "pad") {
         ctx->pad_enable = value != 0;
         ctx->dsc.pad_walk = ctx->pad_ok && ctx->pad_enable ? 1 : 0;
@@ -1974,6 +2045,7 @@ PRC_EXPORT int prc_gpu_evaluate(prc_gpu_ctx* ctx, const prc_gpu_store* store,
     er.legacy = (flags & PRC_EVAL_LEGACY_SCORE) != 0;
     er.deterministic = (flags & PRC_EVAL_DETERMINISTIC) != 0;
     const double scale = (flags & PRC_EVAL_NORMALIZE) && st->n_global ? 1.0 / (double)st->n_global : 1.0;
+    er.grad_scale = scale;
     const unsigned long long key = params_key(ctx, params, st, flags);
     const bool reuse = er.want_grad && ctx->last_fwd_store == st && ctx->last_fwd_gen == ctx->fwd_gen &&
                        ctx->last_fwd_key == key;
@@ -1987,7 +2059,7 @@ PRC_EXPORT int prc_gpu_evaluate(prc_gpu_ctx* ctx, const prc_gpu_store* store,
         cudaStream_t q = ctx->stream;
         for (int i = 0; i < 4; ++i) CK(cudaEventRecord(ctx->ev[i], q));
         EvalArgs ea = eval_args(ctx, st, er, ctx->phong.p);
-        run_gradient(ctx, st, ea);
+        run_gradient(ctx, st, ea, er.per_species ? ctx->dsc.n_species : 1, scale);
         cl = ctx->last_fwd_clamps;
     } else {
         Resolved r = resolve_params(ctx, params, st);
@@ -2002,11 +2074,8 @@ PRC_EXPORT int prc_gpu_evaluate(prc_gpu_ctx* ctx, const prc_gpu_store* store,
     res->grad_kappa = res->grad_gamma = 0.0;
     if (er.want_grad) {
         const int n_out = er.per_species ? s.n_species : 1;
-        if (s.has_medium && (s.unknown >= 0 || er.per_species)) {
-            CK(launch_combine_grad(ctx->g_span.p, ctx->g_vert.p, n_out, ctx->V, scale, ctx->g_out.p,
-                                   ctx->stream, &ctx->launches));
-            copy_out(ctx, res->grad_beta, ctx->g_out.p, (size_t)n_out * ctx->V);
-        }
+        if (s.has_medium && (s.unknown >= 0 || er.per_species) && ctx->grad_res)
+            copy_out(ctx, res->grad_beta, ctx->grad_res, (size_t)n_out * ctx->V);
         double gp[2] = {0, 0};
         CK(cudaMemcpyAsync(gp, ctx->g_phong.p, sizeof gp, cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaEventRecord(ctx->ev[5], ctx->stream));
@@ -2109,14 +2178,12 @@ static double opt_step(prc_gpu_ctx* c, prc_gpu_store* st) {
     ea.weights = c->weights.p;  // K5 with residual weights (+ gradient allreduce)
     ea.per_species = c->opt_per_species && s.has_medium ? 1 : 0;
     ea.do_beta = s.has_medium && (s.unknown >= 0 || ea.per_species) ? 1 : 0;
-    run_gradient(c, st, ea);
+    // per-type mode (config (c)): grad_j = g_span + g_vert[j] for every species j; the
+    // optimiser updates the unknown species' slice
+    run_gradient(c, st, ea, ea.per_species ? s.n_species : 1, scale);
     const double* g;
     if (c->opt_mode == 0) {
-        // per-type mode (config (c)): grad_j = g_span + g_vert[j] for every species j;
-        // the optimiser updates the unknown species' slice
-        const int n_out = ea.per_species ? s.n_species : 1;
-        CK(launch_combine_grad(c->g_span.p, c->g_vert.p, n_out, c->V, scale, c->g_out.p, q, &c->launches));
-        g = c->g_out.p + (ea.per_species ? (size_t)s.unknown * c->V : 0);
+        g = c->grad_res + (ea.per_species ? (size_t)s.unknown * c->V : 0);
     } else {
         CK(launch_scale(c->g_phong.p, 2, scale, q, &c->launches));
         g = c->g_phong.p;
@@ -2306,6 +2373,7 @@ static void set_resolution(prc_gpu_ctx* c, const std::vector<int>& rows, const s
     c->images.alloc((size_t)n_pix);
     c->weights.alloc((size_t)n_pix);
     c->opt_gt.alloc((size_t)n_pix);
+    nvls_setup(c);
     ++c->geo_gen;  // pixel_of changes with the resolution
     ++c->fwd_gen;
 }

@@ -292,3 +292,47 @@ cudaError_t launch_mat_gradient(const DScene& sc, const MatView& mv, const MatCt
 // dst[i] = src[perm[i]]
 cudaError_t launch_gather_u64(const uint32_t* perm, long long n, const unsigned long long* src,
                               unsigned long long* dst, cudaStream_t s, unsigned long long* launches);
+
+// ---- NVLS multicast reduction fused into the K4 / K5 epilogues (prc_nvls.cu) -------
+// out[e] += scale * (span(e) + g_vert[e]) on every rank, e < n_out * V: span(e) sums the
+// padded gradient copies at voxel e mod V (g_pad non-null) or reads g_span[e mod V]; a
+// plain buffer (images) passes only g_span.
+struct NvlsFold {
+    const double* g_pad;
+    int copies;
+    long long stride;
+    const double* g_span;
+    const double* g_vert;
+    int n_out;
+    long long V;
+    int nx, ny, pnx, pnxny;
+    double scale;
+    double* mc;  // set by nvls_fold
+};
+__device__ __forceinline__ double fold_value(const NvlsFold& a, long long e) {
+    const long long v = e % a.V;
+    double s = 0.0;
+    if (a.g_pad) {  // k_unpad_add's sum over the copies
+        const int ix = (int)(v % a.nx), iy = (int)((v / a.nx) % a.ny), iz = (int)(v / ((long long)a.nx * a.ny));
+        const long long pv = (ix + 1) + (long long)a.pnx * (iy + 1) + (long long)a.pnxny * (iz + 1);
+        s = a.g_pad[pv];
+        for (int c = 1; c < a.copies; ++c) s += a.g_pad[(long long)c * a.stride + pv];
+    } else if (a.g_span) {
+        s = a.g_span[v];
+    }
+    if (a.g_vert) s += a.g_vert[e];
+    return s;
+}
+struct NvlsState;
+#include <string>
+typedef struct ncclComm* ncclComm_t;
+// The multicast buffer of n doubles: an NCCL symmetric window with NVLS multimem (world >= 2)
+// or a CUDA multicast object on this device alone (world == 1); `emulate` (world == 1) folds
+// into a plain buffer with atomics instead, to validate the fold where no multicast exists.
+// nullptr + err when the system offers no multicast.
+NvlsState* nvls_create(ncclComm_t comm, int world, int device, size_t n_doubles, bool emulate, std::string* err);
+void nvls_destroy(NvlsState* s);
+double* nvls_local(NvlsState* s);
+size_t nvls_capacity(const NvlsState* s);
+// Zeroes this rank's copy of [offset, offset + n_out V) and adds every rank's fold into it.
+cudaError_t nvls_fold(NvlsState* s, NvlsFold a, size_t offset, cudaStream_t q, unsigned long long* launches);

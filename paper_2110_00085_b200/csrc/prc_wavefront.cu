@@ -291,12 +291,16 @@ __global__ void __launch_bounds__(kFwdTPB, kFwdMinBlocks) k_le_forward(const __g
             if (logval != -INFINITY) {
                 // w, r and geom exactly as event_geometry (the walk's indexing is bit-exact);
                 // a cached surface event needs the ray only for the LE walk
+                double inv_r = 0.0;
                 if (!sv || sc.has_medium) {
                     const V3 to_det = ld3(sc.det[k].pos) - x;
                     r = norm3(to_det);
-                    w = to_det * (1.0 / r);
+                    inv_r = 1.0 / r;
+                    w = to_det * inv_r;
                 }
-                geom = sv ? (double)__int_as_float(vt.ev_c1[e]) : 1.0 / (r * r);
+                // 1/r^2 as (1/r)^2: one division per event instead of two (~1e-16 relative
+                // in the event value; the walk's indexing does not depend on it)
+                geom = sv ? (double)__int_as_float(vt.ev_c1[e]) : inv_r * inv_r;
             }
         } else if (act && (live || !vt.geo_ready)) {
             const DDet& D = sc.det[k];
@@ -541,7 +545,11 @@ __device__ __forceinline__ void red_add_p(bool e, double* a, double x) {
 // (~0.39 per voxel visit for M = 3 at 1e8 paths: the reference DDA on the bench geometry
 // gives 0.53 / 0.39 / 0.31 for M = 2 / 3 / 4 vertices in a 0.3-voxel cube), while `spread` keeps the 32 lanes of a
 // warp on distinct packets far apart in Morton order (no same-address RED conflicts).
-template <int M, bool SC>
+// F: the common scene class of the recycling loop (one species with the fixed-point event
+// term, no surfaces, the default score, one gradient): every interaction vertex is a volume
+// scatter whose score term is 1 / beta_t, so an event needs only its position, the camera
+// and its cached value -- no incoming direction, phase function or surface tests.
+template <int M, bool SC, bool F = false>
 __global__ void __launch_bounds__(kGradTPB, M == 2 ? PRC_GRAD2_MINB : (M == 3 ? PRC_GRAD3_MINB : PRC_GRAD4_MINB)) k_le_gradient_ms(const __grid_constant__ DScene sc,
                                                         const __grid_constant__ VertexTable vt,
                                                         const __grid_constant__ EvalArgs ea,
@@ -575,6 +583,15 @@ __global__ void __launch_bounds__(kGradTPB, M == 2 ? PRC_GRAD2_MINB : (M == 3 ? 
             if (w == 0.0) continue;
             own_acc[r] += w;
             const V3 x = mk(vt.x[i], vt.y[i], vt.z[i]);
+            if constexpr (F) {  // event_geometry's connection (transport.cpp:226-229), nothing else
+                const V3 to_det = ld3(sc.det[k].pos) - x;
+                const double rr = norm3(to_det);
+                S[r].template init<true>(sc, x, to_det * (1.0 / rr), rr);
+                cf[r] = -w;
+                const double bt = (double)ea.sp_t[vt.vox[i]];
+                if (bt > 0.0) acc[r] += w / bt;  // score_term = 1 / beta_t (pathstore.cpp:97-105)
+                continue;
+            }
             const V3 d = mk(vt.dx[i], vt.dy[i], vt.dz[i]);
             const uint32_t meta = vt.meta[i];
             const uint32_t kind = meta_kind(meta);
@@ -916,9 +933,12 @@ cudaError_t launch_le_gradient(const DScene& sc, const VertexTable& vt, const Ev
         if (packet == 2)
             (sc.scache ? k_le_gradient_ms<2, true> : k_le_gradient_ms<2, false>)<<<grid_for(n_pk, kGradTPB), kGradTPB, 0, s>>>(
                 sc, vt, ea, own, spread);
-        else if (packet == 3)
-            (sc.scache ? k_le_gradient_ms<3, true> : k_le_gradient_ms<3, false>)<<<grid_for(n_pk, kGradTPB), kGradTPB, 0, s>>>(
-                sc, vt, ea, own, spread);
+        else if (packet == 3) {
+            const bool fast = sc.c1_fast && !sc.scache && sc.n_surf == 0 && sc.target < 0 && !ea.per_species &&
+                              !ea.legacy && ea.do_beta;
+            (sc.scache ? k_le_gradient_ms<3, true> : fast ? k_le_gradient_ms<3, false, true> : k_le_gradient_ms<3, false>)
+                <<<grid_for(n_pk, kGradTPB), kGradTPB, 0, s>>>(sc, vt, ea, own, spread);
+        }
         else
             (sc.scache ? k_le_gradient_ms<4, true> : k_le_gradient_ms<4, false>)<<<grid_for(n_pk, kGradTPB), kGradTPB, 0, s>>>(
                 sc, vt, ea, own, spread);
