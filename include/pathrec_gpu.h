@@ -415,6 +415,11 @@ int prc_gpu_timer_stop(prc_gpu_ctx* ctx, double* ms);
 /* Device counting pass over a store (no gathers): out[0] events, out[1] live path-span
  * incidences (segments 1..B-1), out[2] LE span incidences, out[3] all path spans. */
 int prc_gpu_store_stats(prc_gpu_ctx* ctx, const prc_gpu_store* store, uint64_t* out4);
+/* Range-check word of a checked build (libpathrec_gpu_checked.so, built with
+ * -DPRC_CHECKED): bit k set when an access of class k left its table (0 padded gathers,
+ * 1 padded reductions, 2 pixel indices, 3 voxel indices, 4 event-cache slots).  Reads and
+ * clears it; *checked_build tells whether this library checks at all (0: flags stay 0). */
+int prc_gpu_debug_checks(prc_gpu_ctx* ctx, uint32_t* flags_out, int* checked_build);
 /* Number of kernels this library launched since ctx creation. */
 int prc_gpu_kernel_launches(const prc_gpu_ctx* ctx, uint64_t* out);
 

@@ -31,6 +31,7 @@ def _nccl_dir() -> str:
 
 
 NCCL_DIR = _nccl_dir()
+CHECKED_OUT = os.path.join(HERE, "libpathrec_gpu_checked.so")  # -DPRC_CHECKED (tests/test_checked.py)
 
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

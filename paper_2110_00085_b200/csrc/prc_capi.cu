@@ -137,6 +137,7 @@ struct prc_gpu_ctx {
     NvlsState* nvls = nullptr;
     DBuf<uint32_t> u32tmp;
     DBuf<int> err;
+    DBuf<unsigned> check;  // DScene::check (checked builds record range violations here)
     void* cub_tmp = nullptr;
     size_t cub_bytes = 0;
     // device-resident optimizer (Algorithm 2)
@@ -526,7 +527,13 @@ void upload_scene(prc_gpu_ctx* c, const prc_scene_desc* d) {
         s.pad_walk = c->pad_ok && c->pad_enable ? 1 : 0;
         s.pnx = s.dims[0] + 2;
         s.pnxny = (s.dims[0] + 2) * (s.dims[1] + 2);
+        s.vpad = (long long)s.pnxny * (long long)(s.dims[2] + 2);
     }
+    if (!c->check.p) {
+        c->check.alloc(1);
+        CK(cudaMemset(c->check.p, 0, sizeof(unsigned)));
+    }
+    s.check = c->check.p;
     c->dsc = s;
     c->V = V;
     c->n_pix = off;
@@ -2663,6 +2670,25 @@ PRC_EXPORT int prc_gpu_store_stats(prc_gpu_ctx* ctx, const prc_gpu_store* store,
     ctx->allreduce_u64(d.p, 4);
     CK(cudaMemcpyAsync(out4, d.p, 32, cudaMemcpyDeviceToHost, ctx->stream));
     ctx->sync();
+    ABI_CATCH
+}
+
+PRC_EXPORT int prc_gpu_debug_checks(prc_gpu_ctx* ctx, uint32_t* flags_out, int* checked_build) {
+    if (!ctx || !flags_out) return fail(PRC_ERR_INVALID, "prc_gpu_debug_checks: null argument");
+#ifdef PRC_CHECKED
+    if (checked_build) *checked_build = 1;
+#else
+    if (checked_build) *checked_build = 0;
+#endif
+    ABI_TRY
+    begin(ctx);
+    *flags_out = 0;
+    if (ctx->check.p) {
+        unsigned f = 0;
+        CK(cudaMemcpy(&f, ctx->check.p, sizeof f, cudaMemcpyDeviceToHost));
+        CK(cudaMemset(ctx->check.p, 0, sizeof f));
+        *flags_out = f;
+    }
     ABI_CATCH
 }
 

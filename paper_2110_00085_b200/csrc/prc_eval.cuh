@@ -10,7 +10,11 @@ namespace prc {
 // fixed-point value floor(v / quantum) as (hi, lo) u64 words: the lo atomic returns the old
 // word, so every wrap-around carries into hi exactly once and the final pair is the exact
 // sum in any order of the additions.
-__device__ __forceinline__ void image_add(const EvalArgs& ea, long long idx, double v) {
+__device__ __forceinline__ void image_add(const DScene& sc, const EvalArgs& ea, long long idx, double v) {
+    PRC_CHECK(sc, idx >= 0 && idx < sc.n_pix, CHK_PIXEL);
+#ifdef PRC_CHECKED
+    if (idx < 0 || idx >= sc.n_pix) return;
+#endif
     if (ea.img_mode == 0) {
         atomicAdd(ea.images + idx, v);
     } else if (ea.img_mode == 1) {

@@ -304,7 +304,7 @@ __global__ void __launch_bounds__(kTPB) k_forward(const __grid_constant__ DScene
                                     ++clamps;
                                 }
                                 const double v = exp(logval) * geom * sc.prefactor;
-                                image_add(ea, D.img_off + pix, v);
+                                image_add(sc, ea, D.img_off + pix, v);
                                 val = (float)v;
                             }
                         } else {

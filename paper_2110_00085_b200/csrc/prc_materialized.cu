@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(kMatTPB) k_mat_forward(const __grid_constant__
                         ++clamps;
                     }
                     val = exp(logval) * mv.e_geom[ei] * sc.prefactor;
-                    image_add(ea, sc.det[mv.e_det[ei]].img_off + mv.e_pix[ei], val);
+                    image_add(sc, ea, sc.det[mv.e_det[ei]].img_off + mv.e_pix[ei], val);
                 }
             }
             mv.e_val[ei] = val;

@@ -223,6 +223,7 @@ __global__ void __launch_bounds__(kFwdTPB, kFwdMinBlocks) k_le_forward(const __g
     const uint32_t kind = meta_kind(meta);
     const int surf = meta_surface(meta);
     const bool live = act && lpv != -INFINITY;
+    PRC_CHECK(sc, !(live && kind == VK_VOLUME) || (vox >= 0 && vox < sc.V), CHK_VOXEL);
     const double den = (live && kind == VK_VOLUME) ? (double)ea.br_tot[vox] : 0.0;
     // lp - log(den) is per vertex: one log per camera event instead of two (the sum is
     // re-associated, a change of ~1e-16 relative in the event value)
@@ -343,7 +344,7 @@ __global__ void __launch_bounds__(kFwdTPB, kFwdMinBlocks) k_le_forward(const __g
         if (SC && direct != 0.0) {
             const double contrib = direct * geom * sc.prefactor;
             val = (float)contrib;
-            if (contrib != 0.0) image_add(ea, sc.det[k].img_off + pix, contrib);
+            if (contrib != 0.0) image_add(sc, ea, sc.det[k].img_off + pix, contrib);
         } else if (logval != -INFINITY) {
             if (sc.has_medium) {
                 logval -= sc.pad_walk ? dda_optical_depth_pad(sc, x, w, r, ea.bt_pad)
@@ -355,7 +356,7 @@ __global__ void __launch_bounds__(kFwdTPB, kFwdMinBlocks) k_le_forward(const __g
             }
             const double contrib = exp(logval) * geom * sc.prefactor;
             val = (float)contrib;
-            if (contrib != 0.0) image_add(ea, sc.det[k].img_off + pix, contrib);
+            if (contrib != 0.0) image_add(sc, ea, sc.det[k].img_off + pix, contrib);
         }
         if (act) {
             vt.ev_val[e] = val;
@@ -433,6 +434,7 @@ __global__ void __launch_bounds__(kWF, PRC_GRAD1_MINB) k_le_gradient(const __gri
             const int pix = vt.ev_pix[(unsigned long long)k * vt.n + i];
             if (pix >= 0) {
                 const double val = (double)vt.ev_val[(unsigned long long)k * vt.n + i];
+                PRC_CHECK(sc, pix >= 0 && sc.det[k].img_off + pix < sc.n_pix, CHK_PIXEL);
                 w = ea.weights ? val * ea.weights[sc.det[k].img_off + pix] : val;
             }
         }
@@ -579,6 +581,7 @@ __global__ void __launch_bounds__(kGradTPB, M == 2 ? PRC_GRAD2_MINB : (M == 3 ? 
             const int pix = vt.ev_pix[(unsigned long long)k * vt.n + i];
             if (pix < 0) continue;
             const double val = (double)vt.ev_val[(unsigned long long)k * vt.n + i];
+            PRC_CHECK(sc, sc.det[k].img_off + pix < sc.n_pix, CHK_PIXEL);
             const double w = ea.weights ? val * ea.weights[sc.det[k].img_off + pix] : val;
             if (w == 0.0) continue;
             own_acc[r] += w;
@@ -588,6 +591,7 @@ __global__ void __launch_bounds__(kGradTPB, M == 2 ? PRC_GRAD2_MINB : (M == 3 ? 
                 const double rr = norm3(to_det);
                 S[r].template init<true>(sc, x, to_det * (1.0 / rr), rr);
                 cf[r] = -w;
+                PRC_CHECK(sc, vt.vox[i] >= 0 && vt.vox[i] < sc.V, CHK_VOXEL);
                 const double bt = (double)ea.sp_t[vt.vox[i]];
                 if (bt > 0.0) acc[r] += w / bt;  // score_term = 1 / beta_t (pathstore.cpp:97-105)
                 continue;
@@ -651,8 +655,8 @@ __global__ void __launch_bounds__(kGradTPB, M == 2 ? PRC_GRAD2_MINB : (M == 3 ? 
                 const int v1 = dda_step_pad(S[1], l1);
                 const double x1 = cf[1] * l1;
                 const bool same = v0 >= 0 && v0 == v1;
-                red_add_if(g, v0, cf[0] * l0 + (same ? x1 : 0.0));
-                red_add_if(g, same ? -1 : v1, x1);
+                RED_ADD_IF(sc, g, ea.g_pad_stride, v0, cf[0] * l0 + (same ? x1 : 0.0));
+                RED_ADD_IF(sc, g, ea.g_pad_stride, same ? -1 : v1, x1);
             }
         } else if (M == 3) {  // hand-scheduled triple (the default packet)
             PRay R0, R1, R2;
@@ -662,9 +666,20 @@ __global__ void __launch_bounds__(kGradTPB, M == 2 ? PRC_GRAD2_MINB : (M == 3 ? 
             auto pstep3 = [&]() {
                 double x0, x1, x2;
                 double *a0, *a1, *a2;
-                const bool e0 = R0.step(x0, a0);
-                const bool e1 = R1.step(x1, a1);
-                const bool e2 = R2.step(x2, a2);
+                bool e0 = R0.step(x0, a0);
+                bool e1 = R1.step(x1, a1);
+                bool e2 = R2.step(x2, a2);
+#ifdef PRC_CHECKED
+                {
+                    const double* hi = g + ea.g_pad_stride;
+                    const bool b0 = e0 && !(a0 >= g && a0 < hi), b1 = e1 && !(a1 >= g && a1 < hi),
+                               b2 = e2 && !(a2 >= g && a2 < hi);
+                    PRC_CHECK(sc, !b0 && !b1 && !b2, CHK_PAD_RED);
+                    e0 = e0 && !b0;
+                    e1 = e1 && !b1;
+                    e2 = e2 && !b2;
+                }
+#endif
                 // same voxel <=> same address; launch_le_gradient runs this packet only on
                 // padded tables below 2^29 voxels (4 GB), so the low 32 bits decide
                 const uint32_t l0 = (uint32_t)(uintptr_t)a0, l1 = (uint32_t)(uintptr_t)a1,
@@ -688,10 +703,10 @@ __global__ void __launch_bounds__(kGradTPB, M == 2 ? PRC_GRAD2_MINB : (M == 3 ? 
                 const bool s10 = v1 == v0, s20 = v2 == v0, s30 = v3 == v0;
                 const bool s21 = v2 == v1 && !s20, s31 = v3 == v1 && !s30;
                 const bool s32 = v3 == v2 && !s30 && !s31;
-                red_add_if(g, v0, cf[0] * l0 + (s10 ? x1 : 0.0) + (s20 ? x2 : 0.0) + (s30 ? x3 : 0.0));
-                red_add_if(g, s10 ? -1 : v1, x1 + (s21 ? x2 : 0.0) + (s31 ? x3 : 0.0));
-                red_add_if(g, (s20 || s21) ? -1 : v2, x2 + (s32 ? x3 : 0.0));
-                red_add_if(g, (s30 || s31 || s32) ? -1 : v3, x3);
+                RED_ADD_IF(sc, g, ea.g_pad_stride, v0, cf[0] * l0 + (s10 ? x1 : 0.0) + (s20 ? x2 : 0.0) + (s30 ? x3 : 0.0));
+                RED_ADD_IF(sc, g, ea.g_pad_stride, s10 ? -1 : v1, x1 + (s21 ? x2 : 0.0) + (s31 ? x3 : 0.0));
+                RED_ADD_IF(sc, g, ea.g_pad_stride, (s20 || s21) ? -1 : v2, x2 + (s32 ? x3 : 0.0));
+                RED_ADD_IF(sc, g, ea.g_pad_stride, (s30 || s31 || s32) ? -1 : v3, x3);
             }
         } else {
             bool any = false;
@@ -721,7 +736,7 @@ __global__ void __launch_bounds__(kGradTPB, M == 2 ? PRC_GRAD2_MINB : (M == 3 ? 
                 any = false;
 #pragma unroll
                 for (int r = 0; r < M; ++r) {
-                    red_add_if(g, v[r], val[r]);
+                    RED_ADD_IF(sc, g, ea.g_pad_stride, v[r], val[r]);
                     any |= S[r].alive;
                 }
             }
@@ -823,7 +838,7 @@ __global__ void PRC_PATHG_LB k_path_gradient(const __grid_constant__ DScene sc,
             for (int u = 0; u < 4; ++u) {
                 double len;
                 const int v = PAD ? dda_step_pad(S, len) : (S.alive ? dda_step_len<false>(S, nx, ny, nz, len) : -1);
-                red_add_if(g, v, cf * len);
+                RED_ADD_IF(sc, g, PAD ? ea.g_pad_stride : sc.V, v, cf * len);
             }
         } while (warp_count(S.alive) >= target && target > 0);
     }
@@ -930,18 +945,17 @@ cudaError_t launch_le_gradient(const DScene& sc, const VertexTable& vt, const Ev
     if (packet == 3 && (long long)sc.pnxny * (long long)(sc.dims[2] + 2) >= (1ll << 29)) packet = 2;
     if (packet > 1) {
         const long long n_pk = ((long long)vt.n + packet - 1) / packet;
+        const bool fast = sc.c1_fast && !sc.scache && sc.n_surf == 0 && sc.target < 0 && !ea.per_species &&
+                          !ea.legacy && ea.do_beta;
         if (packet == 2)
-            (sc.scache ? k_le_gradient_ms<2, true> : k_le_gradient_ms<2, false>)<<<grid_for(n_pk, kGradTPB), kGradTPB, 0, s>>>(
-                sc, vt, ea, own, spread);
-        else if (packet == 3) {
-            const bool fast = sc.c1_fast && !sc.scache && sc.n_surf == 0 && sc.target < 0 && !ea.per_species &&
-                              !ea.legacy && ea.do_beta;
+            (sc.scache ? k_le_gradient_ms<2, true> : fast ? k_le_gradient_ms<2, false, true> : k_le_gradient_ms<2, false>)
+                <<<grid_for(n_pk, kGradTPB), kGradTPB, 0, s>>>(sc, vt, ea, own, spread);
+        else if (packet == 3)
             (sc.scache ? k_le_gradient_ms<3, true> : fast ? k_le_gradient_ms<3, false, true> : k_le_gradient_ms<3, false>)
                 <<<grid_for(n_pk, kGradTPB), kGradTPB, 0, s>>>(sc, vt, ea, own, spread);
-        }
         else
-            (sc.scache ? k_le_gradient_ms<4, true> : k_le_gradient_ms<4, false>)<<<grid_for(n_pk, kGradTPB), kGradTPB, 0, s>>>(
-                sc, vt, ea, own, spread);
+            (sc.scache ? k_le_gradient_ms<4, true> : fast ? k_le_gradient_ms<4, false, true> : k_le_gradient_ms<4, false>)
+                <<<grid_for(n_pk, kGradTPB), kGradTPB, 0, s>>>(sc, vt, ea, own, spread);
         LAUNCH_DONE();
     }
     k_le_gradient<<<grid_for((long long)vt.n, kWF), kWF, 0, s>>>(sc, vt, ea, own, spread);

@@ -119,6 +119,7 @@ def load_library(path: Optional[str] = None):
                               C.POINTER(C.c_int), _dp, C.c_uint64],
         "prc_gpu_last_timings": [vp, _dp],
         "prc_gpu_kernel_launches": [vp, _u64p],
+        "prc_gpu_debug_checks": [vp, _u32p, C.POINTER(C.c_int)],
         "prc_gpu_timer_start": [vp],
         "prc_gpu_timer_stop": [vp, _dp],
         "prc_gpu_store_stats": [vp, vp, _u64p],
@@ -485,6 +486,12 @@ class Context:
         out = np.zeros(4, np.uint64)
         _check(_lib.prc_gpu_store_stats(self.ptr, store.ptr, _ptr(out, _u64p)))
         return dict(zip(["events", "live_path_spans", "le_spans", "path_spans"], out.tolist()))
+
+    def debug_checks(self):
+        """(flags, checked_build): the checked build's range-violation word (read and cleared)."""
+        f, cb = C.c_uint32(), C.c_int()
+        _check(_lib.prc_gpu_debug_checks(self.ptr, C.byref(f), C.byref(cb)))
+        return int(f.value), bool(cb.value)
 
     def kernel_launches(self) -> int:
         n = C.c_uint64()
