@@ -547,11 +547,13 @@ __device__ __forceinline__ void red_add_p(bool e, double* a, double x) {
 // (~0.39 per voxel visit for M = 3 at 1e8 paths: the reference DDA on the bench geometry
 // gives 0.53 / 0.39 / 0.31 for M = 2 / 3 / 4 vertices in a 0.3-voxel cube), while `spread` keeps the 32 lanes of a
 // warp on distinct packets far apart in Morton order (no same-address RED conflicts).
-// F: the common scene class of the recycling loop (one species with the fixed-point event
-// term, no surfaces, the default score, one gradient): every interaction vertex is a volume
-// scatter whose score term is 1 / beta_t, so an event needs only its position, the camera
-// and its cached value -- no incoming direction, phase function or surface tests.
-template <int M, bool SC, bool F = false>
+// F = 1: the common scene class of the recycling loop (one species with the fixed-point
+// event term, no surfaces, the default score, one gradient): every interaction vertex is a
+// volume scatter whose score term is 1 / beta_t, so an event needs only its position, the
+// camera and its cached value -- no incoming direction, phase function or surface tests.
+// F = 2: 2..4 species without surfaces (config (c)): the score terms come from the phase
+// values K4b cached, so again no direction or cos_le is needed.
+template <int M, bool SC, int F = 0>
 __global__ void __launch_bounds__(kGradTPB, M == 2 ? PRC_GRAD2_MINB : (M == 3 ? PRC_GRAD3_MINB : PRC_GRAD4_MINB)) k_le_gradient_ms(const __grid_constant__ DScene sc,
                                                         const __grid_constant__ VertexTable vt,
                                                         const __grid_constant__ EvalArgs ea,
@@ -586,14 +588,31 @@ __global__ void __launch_bounds__(kGradTPB, M == 2 ? PRC_GRAD2_MINB : (M == 3 ? 
             if (w == 0.0) continue;
             own_acc[r] += w;
             const V3 x = mk(vt.x[i], vt.y[i], vt.z[i]);
-            if constexpr (F) {  // event_geometry's connection (transport.cpp:226-229), nothing else
+            if constexpr (F != 0) {  // event_geometry's connection (transport.cpp:226-229), nothing else
                 const V3 to_det = ld3(sc.det[k].pos) - x;
                 const double rr = norm3(to_det);
                 S[r].template init<true>(sc, x, to_det * (1.0 / rr), rr);
                 cf[r] = -w;
-                PRC_CHECK(sc, vt.vox[i] >= 0 && vt.vox[i] < sc.V, CHK_VOXEL);
-                const double bt = (double)ea.sp_t[vt.vox[i]];
-                if (bt > 0.0) acc[r] += w / bt;  // score_term = 1 / beta_t (pathstore.cpp:97-105)
+                const int vox = vt.vox[i];
+                PRC_CHECK(sc, vox >= 0 && vox < sc.V, CHK_VOXEL);
+                if constexpr (F == 1) {
+                    const double bt = (double)ea.sp_t[vox];
+                    if (bt > 0.0) acc[r] += w / bt;  // score_term = 1 / beta_t (pathstore.cpp:97-105)
+                } else {  // score_term (pathstore.cpp:97-105) from the cached phase values
+                    float fj[kFCacheMax];
+                    double num = 0.0;
+                    for (int j = 0; j < sc.n_species; ++j) {
+                        fj[j] = vt.ev_f[((unsigned long long)j * sc.n_det + k) * vt.n + i];
+                        num += sc.sp[j].albedo * (double)ea.sp_t[(long long)j * sc.V + vox] * (double)fj[j];
+                    }
+                    if (num > 0.0) {
+                        if (single)
+                            acc[r] += w * (sc.sp[sc.unknown].albedo * (double)fj[sc.unknown] / num);
+                        else
+                            for (int j = 0; j < sc.n_species; ++j)
+                                atomicAdd(ea.g_vert + (long long)j * sc.V + vox, w * (sc.sp[j].albedo * (double)fj[j] / num));
+                    }
+                }
                 continue;
             }
             const V3 d = mk(vt.dx[i], vt.dy[i], vt.dz[i]);
@@ -945,16 +964,20 @@ cudaError_t launch_le_gradient(const DScene& sc, const VertexTable& vt, const Ev
     if (packet == 3 && (long long)sc.pnxny * (long long)(sc.dims[2] + 2) >= (1ll << 29)) packet = 2;
     if (packet > 1) {
         const long long n_pk = ((long long)vt.n + packet - 1) / packet;
-        const bool fast = sc.c1_fast && !sc.scache && sc.n_surf == 0 && sc.target < 0 && !ea.per_species &&
-                          !ea.legacy && ea.do_beta;
+        // the specialised set-ups (F, above): scenes without surfaces, default score
+        const bool plain = !sc.scache && sc.n_surf == 0 && sc.target < 0 && !ea.legacy && ea.do_beta;
+        const int F = plain && sc.c1_fast && !ea.per_species ? 1 : (plain && sc.fcache && vt.geo_ready ? 2 : 0);
         if (packet == 2)
-            (sc.scache ? k_le_gradient_ms<2, true> : fast ? k_le_gradient_ms<2, false, true> : k_le_gradient_ms<2, false>)
+            (sc.scache ? k_le_gradient_ms<2, true>
+                       : F == 1 ? k_le_gradient_ms<2, false, 1> : F == 2 ? k_le_gradient_ms<2, false, 2> : k_le_gradient_ms<2, false>)
                 <<<grid_for(n_pk, kGradTPB), kGradTPB, 0, s>>>(sc, vt, ea, own, spread);
         else if (packet == 3)
-            (sc.scache ? k_le_gradient_ms<3, true> : fast ? k_le_gradient_ms<3, false, true> : k_le_gradient_ms<3, false>)
+            (sc.scache ? k_le_gradient_ms<3, true>
+                       : F == 1 ? k_le_gradient_ms<3, false, 1> : F == 2 ? k_le_gradient_ms<3, false, 2> : k_le_gradient_ms<3, false>)
                 <<<grid_for(n_pk, kGradTPB), kGradTPB, 0, s>>>(sc, vt, ea, own, spread);
         else
-            (sc.scache ? k_le_gradient_ms<4, true> : fast ? k_le_gradient_ms<4, false, true> : k_le_gradient_ms<4, false>)
+            (sc.scache ? k_le_gradient_ms<4, true>
+                       : F == 1 ? k_le_gradient_ms<4, false, 1> : F == 2 ? k_le_gradient_ms<4, false, 2> : k_le_gradient_ms<4, false>)
                 <<<grid_for(n_pk, kGradTPB), kGradTPB, 0, s>>>(sc, vt, ea, own, spread);
         LAUNCH_DONE();
     }
