@@ -395,9 +395,9 @@ void upload_scene(prc_gpu_ctx* c, const prc_scene_desc* d) {
     if (d->n_species < 0 || d->n_species > PRC_MAX_SPECIES)
         throw Err(PRC_ERR_CONFIG, "scene: species count outside 0..16");
     if (d->n_surfaces < 0 || d->n_surfaces > PRC_MAX_SURF)
-        throw Err(PRC_ERR_CONFIG, "scene: at most 32 surfaces supported");
+        throw Err(PRC_ERR_CONFIG, "scene: at most 64 surfaces supported");
     if (d->n_detectors < 1 || d->n_detectors > PRC_MAX_DET)
-        throw Err(PRC_ERR_CONFIG, "scene: detector count outside 1..32");
+        throw Err(PRC_ERR_CONFIG, "scene: detector count outside 1..64");
     DScene s{};
     s.bmin[0] = d->bounds_min.x;
     s.bmin[1] = d->bounds_min.y;

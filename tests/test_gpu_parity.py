@@ -751,3 +751,25 @@ def test_render_is_bit_reproducible(ctx):
     assert np.array_equal(d1.view(np.uint64), d2.view(np.uint64))
     assert img_err(d1, f) <= 1e-13
     assert img_err(ctx.recycled_render(s, a.store, None), a.images) <= 1e-13
+
+
+def test_many_cameras_and_surfaces(ctx, ref, tmp_path):
+    """More than 32 cameras and surfaces (the engine's inline scene holds up to 64 of
+    each): a device-traced store evaluates like the reference's evaluate_store."""
+    s = S.cloud_scene(8, 6, 6, n_ring=43)  # 44 cameras
+    rng = np.random.default_rng(8)
+    s.surfaces = [S.Surface("sphere", center=tuple(0.15 + 0.7 * rng.random(3)), radius=0.02, brdf="diffuse",
+                            albedo=0.5) for _ in range(40)]
+    assert len(s.detectors) > 32 and len(s.surfaces) > 32
+    ctx.upload(s)
+    st = ctx.render(s, RenderOptions(n_paths=4000, seed=5, keep_paths=True)).store
+    ctx.sort_by_size(st)
+    st.save(str(tmp_path / "many.pstr"))
+    t = perturbed(s)
+    w = np.linspace(-1.0, 2.0, s.pixel_count)
+    a = ctx.evaluate_store(s, st, t, EvalOptions(want_grad=True, pixel_weights=w))
+    b = ref.evaluate(s, str(tmp_path / "many.pstr"), t, abi.PRC_EVAL_NORMALIZE | abi.PRC_EVAL_WANT_GRAD, w)
+    assert img_err(a.images, b["images"]) <= IMG_TOL
+    assert grad_err(a.grad_beta, b["grad"]) <= GRAD_TOL
+    with pytest.raises(PrcConfigError):
+        ctx.upload(S.cloud_scene(8, 4, 4, n_ring=64))  # 65 cameras
