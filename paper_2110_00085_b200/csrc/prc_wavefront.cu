@@ -370,6 +370,60 @@ __global__ void __launch_bounds__(kFwdTPB, kFwdMinBlocks) k_le_forward(const __g
     if ((threadIdx.x & 31) == 0 && clamps) atomicAdd(ea.clamps, (unsigned long long)clamps);
 }
 
+// K4b for the common scene class once the event cache is built: one species with the
+// fixed-point event term, no surfaces, padded walks, geo_ready.  Every interaction vertex
+// is a volume scatter and every event's pixel and c1 come from the cache, so an event is
+// its connection ray, the walk and the exp -- the general kernel's pixel_of, surface,
+// phase and multi-species code is not compiled in (the same expression, the same bits).
+__global__ void __launch_bounds__(kFwdTPB, kFwdMinBlocks) k_le_forward_fast(const __grid_constant__ DScene sc,
+                                                                          const __grid_constant__ VertexTable vt,
+                                                                          const __grid_constant__ EvalArgs ea,
+                                                                          const double* __restrict__ lp) {
+    const unsigned long long i = (unsigned long long)blockIdx.x * kFwdTPB + threadIdx.x;
+    const bool act = i < vt.n;
+    double lvol = -INFINITY;  // lp - log(beta_ref) + log(beta_t), as k_le_forward's lbase / lvol
+    if (act) {
+        const int vox = vt.vox[i];
+        const double lpv = lp[vt.iv[i]];
+        PRC_CHECK(sc, lpv == -INFINITY || (vox >= 0 && vox < sc.V), CHK_VOXEL);
+        if (lpv != -INFINITY) {
+            const double den = (double)ea.br_tot[vox];
+            if (den > 0.0) {
+                const double lbase = lpv - log(den);
+                const double bt = (double)ea.sp_t[vox];
+                if (bt > 0.0) lvol = lbase + log(bt);
+            }
+        }
+    }
+    unsigned clamps = 0;
+    for (int k = 0; k < sc.n_det; ++k) {
+        const unsigned long long e = (unsigned long long)k * vt.n + i;
+        float val = 0.0f;
+        if (lvol != -INFINITY) {
+            const int pix = vt.ev_pix[e];
+            const int32_t q = vt.ev_c1[e];
+            if (pix >= 0 && q != INT32_MIN) {
+                double logval = lvol + c1_dequant(sc, q);
+                const V3 x = mk(vt.x[i], vt.y[i], vt.z[i]);
+                const V3 to_det = ld3(sc.det[k].pos) - x;
+                const double r = norm3(to_det);
+                const double inv_r = 1.0 / r;
+                logval -= dda_optical_depth_pad(sc, x, to_det * inv_r, r, ea.bt_pad);
+                if (logval > PRC_LOG_CLAMP || logval < -PRC_LOG_CLAMP) {
+                    logval = clampd(logval, -PRC_LOG_CLAMP, PRC_LOG_CLAMP);
+                    ++clamps;
+                }
+                const double contrib = exp(logval) * (inv_r * inv_r) * sc.prefactor;
+                val = (float)contrib;
+                if (contrib != 0.0) image_add(sc, ea, sc.det[k].img_off + pix, contrib);
+            }
+        }
+        if (act) vt.ev_val[e] = val;
+    }
+    for (int o = 16; o > 0; o >>= 1) clamps += __shfl_down_sync(0xffffffffu, clamps, o);
+    if ((threadIdx.x & 31) == 0 && clamps) atomicAdd(ea.clamps, (unsigned long long)clamps);
+}
+
 // ------------------------------------------------------------------ K5b LE gradient
 __device__ __forceinline__ double score_j(const DScene& sc, const EvalArgs& ea, int j, int vox,
                                           double c, double num) {
@@ -951,6 +1005,8 @@ cudaError_t launch_le_forward(const DScene& sc, const VertexTable& vt, const Eva
     if (vt.n == 0) return cudaSuccess;
     if (sc.scache)
         k_le_forward<true><<<grid_for((long long)vt.n, kFwdTPB), kFwdTPB, 0, s>>>(sc, vt, ea, lp);
+    else if (vt.geo_ready && sc.c1_fast && sc.n_surf == 0 && sc.pad_walk && sc.has_medium)
+        k_le_forward_fast<<<grid_for((long long)vt.n, kFwdTPB), kFwdTPB, 0, s>>>(sc, vt, ea, lp);
     else
         k_le_forward<false><<<grid_for((long long)vt.n, kFwdTPB), kFwdTPB, 0, s>>>(sc, vt, ea, lp);
     LAUNCH_DONE();
