@@ -17,6 +17,7 @@
 #include <cstring>
 #include <fstream>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -103,6 +104,7 @@ void put3(double* d, H3 v) {
 struct prc_gpu_store;
 
 struct prc_gpu_ctx {
+    std::recursive_mutex mu;  // serialises the calls on this context (begin())
     int device = 0, rank = 0, world = 1;
     ncclComm_t comm = nullptr;
     cudaStream_t stream = nullptr;
@@ -354,7 +356,14 @@ int classify(const std::exception& e) {
     }                                           \
     return PRC_OK;
 
-void begin(prc_gpu_ctx* c) { CK(cudaSetDevice(c->device)); }
+// Every entry point on a context holds its lock for the call: calls on one context are
+// serialised, distinct contexts are independent (SURVEY §8(b) threading; the reference's
+// OptState is single-owner).
+std::unique_lock<std::recursive_mutex> begin(prc_gpu_ctx* c) {
+    std::unique_lock<std::recursive_mutex> lk(c->mu);
+    CK(cudaSetDevice(c->device));
+    return lk;
+}
 
 // ----------------------------------------------------------------------- scene upload
 // Detector::finalize (scene.cpp:8-14) for every detector, at the resolution of the
@@ -1871,7 +1880,7 @@ PRC_EXPORT int prc_gpu_ctx_rank(const prc_gpu_ctx* ctx, int* rank, int* world) {
 PRC_EXPORT int prc_gpu_scene_upload(prc_gpu_ctx* ctx, const prc_scene_desc* scene) {
     if (!ctx || !scene) return fail(PRC_ERR_INVALID, "prc_gpu_scene_upload: null argument");
     ABI_TRY
-    begin(ctx);
+    auto _lk = begin(ctx);
     upload_scene(ctx, scene);
     ABI_CATCH
 }
@@ -1906,7 +1915,7 @@ PRC_EXPORT int prc_gpu_render(prc_gpu_ctx* ctx, const prc_gpu_render_opts* opts,
     if (!ctx || !opts) return fail(PRC_ERR_INVALID, "prc_gpu_render: null argument");
     if (opts->n_paths == 0) return fail(PRC_ERR_CONFIG, "prc_gpu_render: n_paths must be >= 1");
     ABI_TRY
-    begin(ctx);
+    auto _lk = begin(ctx);
     ctx->check_scene();
     const DScene& s = ctx->dsc;
     // bind_params: sampling species values (inverse.cpp:144-150)
@@ -1946,7 +1955,7 @@ PRC_EXPORT int prc_gpu_sort_by_size(prc_gpu_ctx* ctx, prc_gpu_store* store) {
     if (!ctx || !store) return fail(PRC_ERR_INVALID, "prc_gpu_sort_by_size: null argument");
     if (store->ctx != ctx) return fail(PRC_ERR_INVALID, "prc_gpu_sort_by_size: the store belongs to another context");
     ABI_TRY
-    begin(ctx);
+    auto _lk = begin(ctx);
     sort_store(ctx, store);
     ABI_CATCH
 }
@@ -1973,7 +1982,7 @@ PRC_EXPORT int prc_gpu_store_streams(const prc_gpu_store* st, uint64_t* out) {
     if (!st || !out) return fail(PRC_ERR_INVALID, "prc_gpu_store_streams: null argument");
     if (!st->ctx) return fail(PRC_ERR_INVALID, "prc_gpu_store_streams: the store's context was destroyed");
     ABI_TRY
-    begin(st->ctx);
+    auto _lk = begin(st->ctx);
     if (st->n) CK(cudaMemcpy(out, st->stream.p, st->n * 8, cudaMemcpyDeviceToHost));
     ABI_CATCH
 }
@@ -1982,7 +1991,7 @@ PRC_EXPORT int prc_gpu_store_sizes(const prc_gpu_store* st, uint32_t* out) {
     if (!st || !out) return fail(PRC_ERR_INVALID, "prc_gpu_store_sizes: null argument");
     if (!st->ctx) return fail(PRC_ERR_INVALID, "prc_gpu_store_sizes: the store's context was destroyed");
     ABI_TRY
-    begin(st->ctx);
+    auto _lk = begin(st->ctx);
     if (st->n) CK(cudaMemcpy(out, st->B.p, st->n * 4, cudaMemcpyDeviceToHost));
     ABI_CATCH
 }
@@ -1992,7 +2001,7 @@ PRC_EXPORT int prc_gpu_store_export_pstr(prc_gpu_ctx* ctx, const prc_gpu_store* 
     if (!ctx || !store || !path) return fail(PRC_ERR_INVALID, "prc_gpu_store_export_pstr: null argument");
     if (store->ctx != ctx) return fail(PRC_ERR_INVALID, "prc_gpu_store_export_pstr: the store belongs to another context");
     ABI_TRY
-    begin(ctx);
+    auto _lk = begin(ctx);
     ctx->check_scene();
     store_for_scene(ctx, const_cast<prc_gpu_store*>(store));
     export_pstr(ctx, const_cast<prc_gpu_store*>(store), path);
@@ -2002,7 +2011,7 @@ PRC_EXPORT int prc_gpu_store_export_pstr(prc_gpu_ctx* ctx, const prc_gpu_store* 
 PRC_EXPORT int prc_gpu_store_import_pstr(prc_gpu_ctx* ctx, const char* path, prc_gpu_store** out) {
     if (!ctx || !path || !out) return fail(PRC_ERR_INVALID, "prc_gpu_store_import_pstr: null argument");
     ABI_TRY
-    begin(ctx);
+    auto _lk = begin(ctx);
     ctx->check_scene();
     *out = import_pstr(ctx, path, false).release();
     ++ctx->fwd_gen;
@@ -2013,7 +2022,7 @@ PRC_EXPORT int prc_gpu_store_import_pstr_ex(prc_gpu_ctx* ctx, const char* path, 
     if (!ctx || !path || !out) return fail(PRC_ERR_INVALID, "prc_gpu_store_import_pstr_ex: null argument");
     if (flags & ~PRC_IMPORT_MATERIALIZE) return fail(PRC_ERR_CONFIG, "prc_gpu_store_import_pstr_ex: unknown flags");
     ABI_TRY
-    begin(ctx);
+    auto _lk = begin(ctx);
     ctx->check_scene();
     *out = import_pstr(ctx, path, (flags & PRC_IMPORT_MATERIALIZE) != 0).release();
     ++ctx->fwd_gen;
@@ -2042,7 +2051,7 @@ PRC_EXPORT int prc_gpu_evaluate(prc_gpu_ctx* ctx, const prc_gpu_store* store,
         return fail(PRC_ERR_CONFIG, "self_normalize is not supported by the recycling engine");
     if (store->ctx != ctx) return fail(PRC_ERR_INVALID, "prc_gpu_evaluate: the store belongs to another context");
     ABI_TRY
-    begin(ctx);
+    auto _lk = begin(ctx);
     ctx->check_scene();
     auto* st = const_cast<prc_gpu_store*>(store);
     store_for_scene(ctx, st);
@@ -2209,7 +2218,7 @@ PRC_EXPORT int prc_gpu_opt_init(prc_gpu_ctx* ctx, const prc_gpu_params* initial,
                                 const double* gt_images, const prc_gpu_adam_config* adam) {
     if (!ctx || !gt_images) return fail(PRC_ERR_INVALID, "prc_gpu_opt_init: null argument");
     ABI_TRY
-    begin(ctx);
+    auto _lk = begin(ctx);
     ctx->check_scene();
     opt_init(ctx, initial, gt_images, adam);
     ABI_CATCH
@@ -2220,7 +2229,7 @@ PRC_EXPORT int prc_gpu_opt_step(prc_gpu_ctx* ctx, const prc_gpu_store* store, do
     if (!ctx->opt_ready) return fail(PRC_ERR_INVALID, "prc_gpu_opt_step: optimizer not initialised");
     if (store->ctx != ctx) return fail(PRC_ERR_INVALID, "prc_gpu_opt_step: the store belongs to another context");
     ABI_TRY
-    begin(ctx);
+    auto _lk = begin(ctx);
     ctx->check_scene();
     store_for_scene(ctx, const_cast<prc_gpu_store*>(store));
     const double l = opt_step(ctx, const_cast<prc_gpu_store*>(store));
@@ -2233,7 +2242,7 @@ PRC_EXPORT int prc_gpu_opt_adam_step(prc_gpu_ctx* ctx, const double* grad, uint6
     if (!ctx->opt_ready) return fail(PRC_ERR_INVALID, "prc_gpu_opt_adam_step: optimizer not initialised");
     if ((long long)n != ctx->opt_n) return fail(PRC_ERR_CONFIG, "prc_gpu_opt_adam_step: gradient size != unknowns");
     ABI_TRY
-    begin(ctx);
+    auto _lk = begin(ctx);
     DBuf<double> g;
     g.alloc((size_t)n);
     CK(cudaMemcpyAsync(g.p, grad, (size_t)n * 8, cudaMemcpyHostToDevice, ctx->stream));
@@ -2246,7 +2255,7 @@ PRC_EXPORT int prc_gpu_opt_params(prc_gpu_ctx* ctx, double* beta_out, double* ka
     if (!ctx) return fail(PRC_ERR_INVALID, "prc_gpu_opt_params: null argument");
     if (!ctx->opt_ready) return fail(PRC_ERR_INVALID, "optimizer not initialised");
     ABI_TRY
-    begin(ctx);
+    auto _lk = begin(ctx);
     if (ctx->opt_mode == 0) {
         copy_out(ctx, beta_out, ctx->opt_x.p, (size_t)ctx->V);
         if (kappa_s) *kappa_s = ctx->scene_kappa;
@@ -2265,7 +2274,7 @@ PRC_EXPORT int prc_gpu_opt_params(prc_gpu_ctx* ctx, double* beta_out, double* ka
 PRC_EXPORT int prc_gpu_opt_images(prc_gpu_ctx* ctx, double* images_out) {
     if (!ctx || !images_out) return fail(PRC_ERR_INVALID, "prc_gpu_opt_images: null argument");
     ABI_TRY
-    begin(ctx);
+    auto _lk = begin(ctx);
     copy_out(ctx, images_out, ctx->images.p, (size_t)ctx->n_pix);
     ctx->sync();
     ABI_CATCH
@@ -2278,7 +2287,7 @@ PRC_EXPORT int prc_gpu_reconstruct(prc_gpu_ctx* ctx, const prc_gpu_params* initi
     if (!ctx || !gt_images || !o) return fail(PRC_ERR_INVALID, "prc_gpu_reconstruct: null argument");
     if (o->n_paths == 0) return fail(PRC_ERR_CONFIG, "reconstruct: n_paths must be >= 1");
     ABI_TRY
-    begin(ctx);
+    auto _lk = begin(ctx);
     ctx->check_scene();
     opt_init(ctx, initial, gt_images, adam);
     const int n_r = std::max(1, o->recycle_period);
@@ -2393,7 +2402,7 @@ PRC_EXPORT int prc_gpu_reconstruct_schedule(prc_gpu_ctx* ctx, const prc_gpu_para
     if (sch->n_stages < 1 || !sch->stages)
         return fail(PRC_ERR_CONFIG, "reconstruct: schedule needs at least one stage");
     ABI_TRY
-    begin(ctx);
+    auto _lk = begin(ctx);
     ctx->check_scene();
     const auto t_start = std::chrono::steady_clock::now();
     const int n_det = ctx->dsc.n_det;
@@ -2520,7 +2529,7 @@ PRC_EXPORT int prc_gpu_space_carve(prc_gpu_ctx* ctx, const double* gt_images, do
                                    double fill_extinction, uint8_t* mask_out, double* beta_out) {
     if (!ctx || !gt_images) return fail(PRC_ERR_INVALID, "prc_gpu_space_carve: null argument");
     ABI_TRY
-    begin(ctx);
+    auto _lk = begin(ctx);
     ctx->check_scene();
     const DScene& s = ctx->dsc;
     if (s.n_det < 2) throw Err(PRC_ERR_INVALID, "space_carve: needs at least 2 detectors");
@@ -2634,7 +2643,7 @@ PRC_EXPORT int prc_gpu_last_timings(const prc_gpu_ctx* ctx, double* ms8) {
 PRC_EXPORT int prc_gpu_timer_start(prc_gpu_ctx* ctx) {
     if (!ctx) return fail(PRC_ERR_INVALID, "null argument");
     ABI_TRY
-    begin(ctx);
+    auto _lk = begin(ctx);
     if (!ctx->timer[0]) {
         CK(cudaEventCreate(&ctx->timer[0]));
         CK(cudaEventCreate(&ctx->timer[1]));
@@ -2646,7 +2655,7 @@ PRC_EXPORT int prc_gpu_timer_start(prc_gpu_ctx* ctx) {
 PRC_EXPORT int prc_gpu_timer_stop(prc_gpu_ctx* ctx, double* ms) {
     if (!ctx || !ms || !ctx->timer[0]) return fail(PRC_ERR_INVALID, "timer not started");
     ABI_TRY
-    begin(ctx);
+    auto _lk = begin(ctx);
     CK(cudaEventRecord(ctx->timer[1], ctx->stream));
     CK(cudaEventSynchronize(ctx->timer[1]));
     float f = 0.f;
@@ -2659,7 +2668,7 @@ PRC_EXPORT int prc_gpu_store_stats(prc_gpu_ctx* ctx, const prc_gpu_store* store,
     if (!ctx || !store || !out4) return fail(PRC_ERR_INVALID, "null argument");
     if (store->ctx != ctx) return fail(PRC_ERR_INVALID, "prc_gpu_store_stats: the store belongs to another context");
     ABI_TRY
-    begin(ctx);
+    auto _lk = begin(ctx);
     ctx->check_scene();
     store_for_scene(ctx, const_cast<prc_gpu_store*>(store));
     DBuf<unsigned long long> d;
@@ -2681,7 +2690,7 @@ PRC_EXPORT int prc_gpu_debug_checks(prc_gpu_ctx* ctx, uint32_t* flags_out, int* 
     if (checked_build) *checked_build = 0;
 #endif
     ABI_TRY
-    begin(ctx);
+    auto _lk = begin(ctx);
     *flags_out = 0;
     if (ctx->check.p) {
         unsigned f = 0;
@@ -2702,7 +2711,7 @@ PRC_EXPORT int prc_gpu_debug_philox(prc_gpu_ctx* ctx, uint64_t seed, uint64_t st
                                     uint32_t* out) {
     if (!ctx || !out) return fail(PRC_ERR_INVALID, "null argument");
     ABI_TRY
-    begin(ctx);
+    auto _lk = begin(ctx);
     DBuf<uint32_t> d;
     d.alloc(std::max<uint64_t>(n, 1));
     CK(launch_philox(seed, stream, n, d.p, ctx->stream, &ctx->launches));
@@ -2715,7 +2724,7 @@ static int debug_walk(prc_gpu_ctx* ctx, uint64_t n, const double* rays, uint32_t
                       uint32_t* voxels_out, double* lengths_out, uint64_t cap, bool pad) {
     if (!ctx || !rays || !counts_out) return fail(PRC_ERR_INVALID, "null argument");
     ABI_TRY
-    begin(ctx);
+    auto _lk = begin(ctx);
     ctx->check_scene();
     if (!ctx->dsc.has_medium) throw Err(PRC_ERR_CONFIG, "scene has no medium grid");
     if (pad && !ctx->pad_ok) throw Err(PRC_ERR_CONFIG, "padded walks are not valid for this scene");
@@ -2763,7 +2772,7 @@ PRC_EXPORT int prc_gpu_debug_pixel_of(prc_gpu_ctx* ctx, int det, uint64_t n, con
                                       int32_t* out) {
     if (!ctx || !pts || !out) return fail(PRC_ERR_INVALID, "null argument");
     ABI_TRY
-    begin(ctx);
+    auto _lk = begin(ctx);
     ctx->check_scene();
     if (det < 0 || det >= ctx->dsc.n_det) throw Err(PRC_ERR_INVALID, "detector index out of range");
     cudaStream_t q = ctx->stream;

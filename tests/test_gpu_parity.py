@@ -773,3 +773,46 @@ def test_many_cameras_and_surfaces(ctx, ref, tmp_path):
     assert grad_err(a.grad_beta, b["grad"]) <= GRAD_TOL
     with pytest.raises(PrcConfigError):
         ctx.upload(S.cloud_scene(8, 4, 4, n_ring=64))  # 65 cameras
+
+
+def test_render_without_images_traces_only(ctx):
+    """prc_gpu_render with images NULL (reconstruct's resample): the same store, no fresh
+    evaluation."""
+    s = S.cloud_scene(12, 10, 10)
+    ctx.upload(s)
+    a = ctx.render(s, RenderOptions(n_paths=30_000, seed=9, keep_paths=True))
+    n0 = ctx.kernel_launches()
+    b = ctx.render(s, RenderOptions(n_paths=30_000, seed=9, keep_paths=True, images=False))
+    assert b.images is None
+    assert np.array_equal(a.store.sizes(), b.store.sizes()) and a.truncated_paths == b.truncated_paths
+    assert img_err(ctx.recycled_render(s, b.store, None), a.images) <= 1e-12
+    assert ctx.kernel_launches() - n0 > 0
+
+
+def test_concurrent_calls_on_one_context_are_serialised(ctx, golden_dir):
+    """Calls on one context are serialised by the context (SURVEY §8(b) threading): four
+    host threads evaluating through the same context get the single-thread results."""
+    import threading
+    scene = FIXTURES["tomo2"]["scene"]()
+    ctx.upload(scene)
+    st = ctx.load_store(str(golden_dir / "tomo2.pstr"))
+    w = weight_patterns(scene)["w"]
+    params = [perturbed(scene), None]
+    want = [ctx.evaluate_store(scene, st, p, EvalOptions(want_grad=True, pixel_weights=w)) for p in params]
+    out, errs = {}, []
+
+    def run(k):
+        try:
+            for it in range(5):
+                out[(k, it)] = ctx.evaluate_store(scene, st, params[k % 2], EvalOptions(want_grad=True, pixel_weights=w))
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+    th = [threading.Thread(target=run, args=(k,)) for k in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for (k, it), r in out.items():
+        assert img_err(r.images, want[k % 2].images) <= 1e-12
+        assert grad_err(r.grad_beta, want[k % 2].grad_beta) <= 1e-12
