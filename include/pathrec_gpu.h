@@ -177,7 +177,11 @@ int prc_gpu_ctx_rank(const prc_gpu_ctx* ctx, int* rank, int* world);
  * off the guard-free walks over the padded voxel layout (default 1; same results);
  * "grad_copies" = copies of the padded gradient the gradient kernel reduces into (0 =
  * default: 8, fewer when they would exceed 2 GB; applied at the next scene upload; same
- * results up to the order of floating-point sums). */
+ * results up to the order of floating-point sums); "events" 0 turns off the compact
+ * event list of scenes without a medium (default 1: after the first forward over a store,
+ * forwards and gradients run over its events only; same event values); "nvls" 1 =
+ * images and gradients reduced over ranks by NVLS multicast (2 = the fold without
+ * multicast, one rank; applied at the next scene upload). */
 int prc_gpu_ctx_set_option(prc_gpu_ctx* ctx, const char* key, int64_t value);
 
 /* Uploads (and validates, finalizes) the scene; replaces any previous scene and

@@ -114,6 +114,7 @@ struct prc_gpu_ctx {
     int spread = 64;     // K5b lane spreading factor (measured at 1e8: 64-128 best; 16 +10%, 1 +25%)
     int opt_per_species = 0;  // opt_step computes per-type gradients of every species
     int packet = 3;      // K5b rays per thread walked in lockstep (measured best: 3)
+    bool evc_enable = true;  // event list for scenes without a medium (option "events")
     bool pad_ok = false, pad_enable = true;  // guard-free padded walks valid / allowed
     // scene
     bool have_scene = false;
@@ -212,6 +213,17 @@ struct prc_gpu_store {
     DBuf<float> ev_f;      // wavefront, 2..4 species: phase values (VertexTable::ev_f)
     unsigned long long geo_key = 0;  // == ctx geo_gen while ev_pix / ev_c1 hold the geometry
     DBuf<double> lp, own;  // per interaction vertex: log-prefix (K4a), weight sum (K5b)
+    // event list of scenes without a medium (EventList, prc_kernels.cuh); valid while
+    // evc_key == geo_key == ctx geo_gen
+    unsigned long long evc_key = 0, n_evc = 0;
+    bool evc_vals = false;  // the last forward's event values are in evc_val (K4b')
+    DBuf<unsigned long long> evc_off;
+    DBuf<uint32_t> evc_iv;
+    DBuf<int32_t> evc_px;
+    DBuf<double> evc_lobe;
+    DBuf<float> evc_geom, evc_val;
+    DBuf<uint8_t> evc_surf;
+    DBuf<double> evc_vlobe;  // EvalArgs::vlobe, per interaction-vertex slot
     bool vt_ready = false; // Morton-ordered vertex table (wavefront mapping)
     DBuf<double> vt_x, vt_y, vt_z, vt_dx, vt_dy, vt_dz;
     DBuf<int32_t> vt_vox;
@@ -323,7 +335,8 @@ struct prc_gpu_store {
         return mat_device_bytes() + B.bytes() + stride.bytes() + stream.bytes() + rec_base.bytes() + iv_base.bytes() +
                trunc.bytes() + px.bytes() * 8 + vox.bytes() + meta.bytes() + ev_val.bytes() +
                ev_pix.bytes() + ev_c1.bytes() + ev_f.bytes() + br_tot64.bytes() + sp_ref.bytes() + br_tot.bytes() + lp.bytes() +
-               own.bytes() + vt_x.bytes() * 6 + vt_vox.bytes() + vt_meta.bytes() + vt_iv.bytes();
+               own.bytes() + vt_x.bytes() * 6 + vt_vox.bytes() + vt_meta.bytes() + vt_iv.bytes() + evc_off.bytes() +
+               evc_iv.bytes() + evc_px.bytes() + evc_lobe.bytes() + evc_geom.bytes() + evc_val.bytes() + evc_surf.bytes() + evc_vlobe.bytes();
     }
 };
 
@@ -803,6 +816,66 @@ VertexTable vertex_table(prc_gpu_store* st) {
     return v;
 }
 
+// Scenes without a medium evaluate over the event list (EventList): surface events only,
+// int32 image indices, at most 255 surfaces.
+bool evc_applies(const prc_gpu_ctx* c) {
+    const DScene& s = c->dsc;
+    return c->evc_enable && c->mode == 0 && !s.has_medium && s.scache && s.n_surf <= 255 &&
+           c->n_pix < (1ll << 31);
+}
+
+bool evc_ready(const prc_gpu_ctx* c, const prc_gpu_store* st) {
+    return evc_applies(c) && st->geo_key == c->geo_gen && st->evc_key == c->geo_gen;
+}
+
+EventList event_list(prc_gpu_store* st) {
+    EventList el{};
+    el.n = st->n_evc;
+    el.n_iv = st->n_iv;
+    el.off = st->evc_off.p;
+    el.iv = st->evc_iv.p;
+    el.px = st->evc_px.p;
+    el.lobe = st->evc_lobe.p;
+    el.geom = st->evc_geom.p;
+    el.surf = st->evc_surf.p;
+    el.val = st->evc_val.p;
+    return el;
+}
+
+// (Re)builds the event list from the dense cache a forward over the store just wrote.
+// Called after every dense pass: whatever invalidated the list (a new geometry
+// generation, a re-sorted store with its rebuilt vertex table) also sent this forward
+// down the dense path.
+void build_event_list(prc_gpu_ctx* c, prc_gpu_store* st) {
+    st->evc_key = 0;
+    if (!evc_applies(c) || st->geo_key != c->geo_gen) return;
+    cudaStream_t q = c->stream;
+    const size_t niv = (size_t)st->n_iv;
+    st->evc_off.grow(niv + 1);
+    DBuf<unsigned long long> cnt;
+    cnt.alloc(niv + 1);
+    CK(cudaMemsetAsync(cnt.p, 0, cnt.bytes(), q));
+    const VertexTable vt = vertex_table(st);
+    CK(launch_evc_count(c->dsc, vt, cnt.p, q, &c->launches));
+    CK(scan_u64(cnt.p, st->evc_off.p, (long long)niv + 1, &c->cub_tmp, &c->cub_bytes, q));
+    unsigned long long n = 0;
+    CK(cudaMemcpyAsync(&n, st->evc_off.p + niv, 8, cudaMemcpyDeviceToHost, q));
+    c->sync();
+    const size_t nn = (size_t)std::max<unsigned long long>(n, 1);
+    st->evc_iv.grow(nn);
+    st->evc_px.grow(nn);
+    st->evc_lobe.grow(nn);
+    st->evc_geom.grow(nn);
+    st->evc_val.grow(nn);
+    st->evc_surf.grow(nn);
+    CK(launch_evc_fill(c->dsc, vt, st->evc_off.p, st->evc_iv.p, st->evc_px.p, st->evc_lobe.p, st->evc_geom.p,
+                       st->evc_surf.p, q, &c->launches));
+    st->evc_vlobe.grow(std::max<size_t>(niv, 1));
+    CK(launch_vlobe(c->dsc, st->view(), st->evc_vlobe.p, q, &c->launches));
+    st->n_evc = n;
+    st->evc_key = c->geo_gen;
+}
+
 EvalArgs eval_args(prc_gpu_ctx* c, prc_gpu_store* st, const EvalRun& er, const double* phong_dev) {
     const DScene& s = c->dsc;
     EvalArgs ea{};
@@ -826,6 +899,7 @@ EvalArgs eval_args(prc_gpu_ctx* c, prc_gpu_store* st, const EvalRun& er, const d
     ea.per_species = er.per_species ? 1 : 0;
     ea.legacy = er.legacy ? 1 : 0;
     ea.do_beta = s.has_medium && (s.unknown >= 0 || er.per_species) ? 1 : 0;
+    ea.vlobe = evc_ready(c, st) ? st->evc_vlobe.p : nullptr;
     return ea;
 }
 
@@ -951,10 +1025,19 @@ void run_forward(prc_gpu_ctx* c, prc_gpu_store* st, const Resolved& r, const Eva
     if (c->mode == 0) {
         CK(launch_prefix(s, st->view(), ea, st->lp.p, q, &c->launches));
         CK(cudaEventRecord(c->ev[6], q));
-        image_pass(c, ea, er, [&](const EvalArgs& a) {
-            CK(launch_le_forward(s, vertex_table(st), a, st->lp.p, q, &c->launches));
-            st->geo_key = c->geo_gen;  // K4b wrote the event geometry (stream-ordered for later launches)
-        });
+        if (evc_ready(c, st)) {
+            image_pass(c, ea, er, [&](const EvalArgs& a) {
+                CK(launch_evc_forward(s, event_list(st), a, st->lp.p, q, &c->launches));
+            });
+            st->evc_vals = true;
+        } else {
+            image_pass(c, ea, er, [&](const EvalArgs& a) {
+                CK(launch_le_forward(s, vertex_table(st), a, st->lp.p, q, &c->launches));
+                st->geo_key = c->geo_gen;  // K4b wrote the event geometry (stream-ordered for later launches)
+            });
+            st->evc_vals = false;  // this pass's event values are in the dense cache
+            build_event_list(c, st);  // later forwards over the store take the event list
+        }
     } else {
         st->geo_key = 0;  // the per-path kernels reuse ev_pix in path layout
         image_pass(c, ea, er, [&](const EvalArgs& a) { CK(launch_forward(s, st->view(), a, q, &c->launches)); });
@@ -980,8 +1063,11 @@ void run_gradient(prc_gpu_ctx* c, prc_gpu_store* st, const EvalArgs& ea, int n_o
         if (s.pad_walk) CK(cudaMemsetAsync(c->g_pad.p, 0, c->g_pad.bytes(), q));
         // lane spreading only de-conflicts the LE-span reductions; without them (no medium,
         // or no beta gradient) lanes take consecutive vertices so the event loads coalesce
-        CK(launch_le_gradient(s, vertex_table(st), ea, st->own.p, ea.do_beta ? c->spread : 1,
-                              s.pad_walk ? c->packet : 1, q, &c->launches));
+        if (evc_ready(c, st) && st->evc_vals)
+            CK(launch_evc_gradient(s, event_list(st), ea, st->own.p, q, &c->launches));
+        else
+            CK(launch_le_gradient(s, vertex_table(st), ea, st->own.p, ea.do_beta ? c->spread : 1,
+                                  s.pad_walk ? c->packet : 1, q, &c->launches));
         CK(cudaEventRecord(c->ev[7], q));
         c->timed_grad = true;
         CK(launch_path_gradient(s, st->view(), ea, st->own.p, q, &c->launches));
@@ -1859,6 +1945,8 @@ PRC_EXPORT int prc_gpu_ctx_set_option(prc_gpu_ctx* ctx, const char* key, int64_t
         if (value < 0 || value > 2) return fail(PRC_ERR_CONFIG, "nvls must be 0, 1 or 2");
         ctx->nvls_enable = value != 0;
         ctx->nvls_emulate = value == 2;
+    } else if (k == "events") {
+        ctx->evc_enable = value != 0;
     } else if (k == "pad") {
         ctx->pad_enable = value != 0;
         ctx->dsc.pad_walk = ctx->pad_ok && ctx->pad_enable ? 1 : 0;

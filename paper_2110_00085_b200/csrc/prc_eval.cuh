@@ -144,16 +144,48 @@ __device__ __forceinline__ void vertex_scores(const DScene& sc, const EvalArgs& 
     }
 }
 
-__device__ __forceinline__ void phong_scores(const double* phong, double c, double wgt, double& gk,
-                                             double& gg) {  // brdf.hpp:21-30
+// d_kappa / d_gamma of the Phong lobe over f_r (brdf.hpp:21-30) from lc = log(clamp(c, 0, 1)).
+__device__ __forceinline__ void phong_scores_lc(const double* phong, double lc, double wgt, double& gk,
+                                                double& gg) {
     const double kap = phong[0], gam = phong[1];
-    const double cc = clampd(c, 0.0, 1.0);
-    const double pw = pow(cc, gam);
+    const double pw = pow01(lc, gam);
     const double fr = 1.0 - kap + kap * pw;
     if (fr > 0.0) {
         gk += wgt * (-1.0 + pw) / fr;
-        gg += wgt * (cc <= 0.0 ? 0.0 : kap * pw * log(cc)) / fr;
+        gg += wgt * (lc == -INFINITY ? 0.0 : kap * pw * lc) / fr;
     }
+}
+// Adds (a, b) over the CTA into dst[0], dst[1]: warp shuffles, then one pair of fp64
+// reductions per CTA (per-warp reductions into two addresses serialise at L2).  Every
+// thread of the CTA must call it.
+template <int TPB>
+__device__ __forceinline__ void cta_add2(double a, double b, double* dst) {
+    __shared__ double sa[TPB / 32], sb[TPB / 32];
+    for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_down_sync(0xffffffffu, a, o);
+        b += __shfl_down_sync(0xffffffffu, b, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        sa[threadIdx.x >> 5] = a;
+        sb[threadIdx.x >> 5] = b;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double x = 0.0, y = 0.0;
+        for (int r = 0; r < TPB / 32; ++r) {
+            x += sa[r];
+            y += sb[r];
+        }
+        if (x != 0.0 || y != 0.0) {
+            atomicAdd(dst, x);
+            atomicAdd(dst + 1, y);
+        }
+    }
+}
+
+__device__ __forceinline__ void phong_scores(const double* phong, double c, double wgt, double& gk,
+                                             double& gg) {  // brdf.hpp:21-30
+    phong_scores_lc(phong, log(clampd(c, 0.0, 1.0)), wgt, gk, gg);
 }
 
 

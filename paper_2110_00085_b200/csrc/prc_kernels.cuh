@@ -96,6 +96,11 @@ struct EvalArgs {
     unsigned long long* img_max;
     unsigned long long* img_fx;
     double img_inv_quantum;
+    // Scenes on the event list (no medium): per interaction-vertex slot, the surface
+    // vertex's continuation lobe term -- the target surface's lc = log(clamp(cos, 0, 1)),
+    // any other surface's log(pi f_r(cos)) (-inf: f_r <= 0); NULL elsewhere.  K4a / K5a
+    // then skip the fixed surfaces' BRDF and logs (the same values, cached).
+    const double* vlobe;
 };
 
 struct TraceArgs {
@@ -219,6 +224,38 @@ cudaError_t launch_le_forward(const DScene& sc, const VertexTable& vt, const Eva
 cudaError_t launch_le_gradient(const DScene& sc, const VertexTable& vt, const EvalArgs& ea,
                                double* own, int spread, int packet, cudaStream_t s,
                                unsigned long long* launches);
+// Event list of a scene without a medium (reflectometry, config (d)): no LE walks, so an
+// event is a BRDF evaluation, one image reduction and its weight -- and most (vertex,
+// camera) slots of the dense [det][i] cache hold no event (a surface point faces few
+// cameras).  Built once per store geometry from that cache, in interaction-vertex order
+// (events of one vertex contiguous, cameras ascending): the log-prefix gathers of K4b'
+// and the weight sums of K5b' run along lp / own.
+struct EventList {
+    unsigned long long n, n_iv;
+    const unsigned long long* off;  // [n_iv + 1]: events of slot iv are [off[iv], off[iv + 1])
+    const uint32_t* iv;             // interaction-vertex slot of the event
+    const int32_t* px;              // image index img_off[det] + pixel
+    // the target surface's events: lc = log(clamp(cos_le, 0, 1)) (pow01); other surfaces
+    // (fixed BRDF): the BRDF value f_r(cos_le) itself
+    const double* lobe;
+    const float* geom;              // cached f32 geometry factor
+    const uint8_t* surf;            // surface id
+    float* val;                     // event value, K4b' -> K5b'
+};
+// cnt[iv] = events of slot iv (cnt zeroed by the caller, n_iv + 1 entries).
+cudaError_t launch_evc_count(const DScene& sc, const VertexTable& vt, unsigned long long* cnt, cudaStream_t s,
+                             unsigned long long* launches);
+cudaError_t launch_evc_fill(const DScene& sc, const VertexTable& vt, const unsigned long long* off, uint32_t* iv,
+                            int32_t* px, double* lobe, float* geom, uint8_t* surf, cudaStream_t s,
+                            unsigned long long* launches);
+// EvalArgs::vlobe of every interaction vertex of the store (thread per path).
+cudaError_t launch_vlobe(const DScene& sc, const StoreView& st, double* vlobe, cudaStream_t s,
+                         unsigned long long* launches);
+// K4b' and K5b' (thread per event) over the event list.
+cudaError_t launch_evc_forward(const DScene& sc, const EventList& el, const EvalArgs& ea, const double* lp,
+                               cudaStream_t s, unsigned long long* launches);
+cudaError_t launch_evc_gradient(const DScene& sc, const EventList& el, const EvalArgs& ea, double* own,
+                                cudaStream_t s, unsigned long long* launches);
 // K5a: per-path suffix pass (segment spans, continuation scores) from own[iv].
 cudaError_t launch_path_gradient(const DScene& sc, const StoreView& st, const EvalArgs& ea,
                                  const double* own, cudaStream_t s, unsigned long long* launches);

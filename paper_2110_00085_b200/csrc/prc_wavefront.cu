@@ -21,6 +21,8 @@
 // All voxel indexing goes through the bit-exact fp64 DDA of prc_device.cuh.
 #include <cub/device/device_radix_sort.cuh>
 
+#include <algorithm>
+
 #include "prc_eval.cuh"
 
 using namespace prc;
@@ -151,7 +153,8 @@ __global__ void PRC_PREFIX_LB k_prefix(const __grid_constant__ DScene sc,
     if (B < 2) return;
     const unsigned long long rb = st.rec_base[p], ib = st.iv_base[p];
     const unsigned rs = st.stride[p];
-    V3 xprev = mk(st.px[rb], st.py[rb], st.pz[rb]);
+    const bool med = sc.has_medium;  // without a medium the positions are not needed
+    V3 xprev = med ? mk(st.px[rb], st.py[rb], st.pz[rb]) : mk(0.0, 0.0, 0.0);
     double l = 0.0;
     bool dead = false;
     for (int b = 1; b < B; ++b) {
@@ -188,13 +191,28 @@ __global__ void PRC_PREFIX_LB k_prefix(const __grid_constant__ DScene sc,
                     l += log(num) - log(den);
             }
         } else if (kind == VK_SURFACE) {
-            const double fr = surf_brdf(sc, ea.phong, meta_surface(m), ct);
-            if (fr <= 0.0)
-                dead = true;
-            else
-                l += log(PRC_PI * fr);
+            if (ea.vlobe) {  // cached lobe term (EventList scenes): the same values
+                const double vl = ea.vlobe[iv];
+                if (meta_surface(m) == sc.target) {
+                    const double fr = 1.0 - ea.phong[0] + ea.phong[0] * pow01(vl, ea.phong[1]);
+                    if (fr <= 0.0)
+                        dead = true;
+                    else
+                        l += log(PRC_PI * fr);
+                } else if (vl == -INFINITY) {
+                    dead = true;
+                } else {
+                    l += vl;
+                }
+            } else {
+                const double fr = surf_brdf(sc, ea.phong, meta_surface(m), ct);
+                if (fr <= 0.0)
+                    dead = true;
+                else
+                    l += log(PRC_PI * fr);
+            }
         }
-        xprev = mk(st.px[r], st.py[r], st.pz[r]);
+        if (med) xprev = mk(st.px[r], st.py[r], st.pz[r]);
     }
 }
 
@@ -533,16 +551,7 @@ __global__ void __launch_bounds__(kWF, PRC_GRAD1_MINB) k_le_gradient(const __gri
         own[vt.iv[i]] = own_acc;
         if (single && acc != 0.0) atomicAdd(ea.g_vert + vox, acc);
     }
-    if (sc.target >= 0) {
-        for (int o = 16; o > 0; o >>= 1) {
-            gk += __shfl_down_sync(0xffffffffu, gk, o);
-            gg += __shfl_down_sync(0xffffffffu, gg, o);
-        }
-        if ((threadIdx.x & 31) == 0 && (gk != 0.0 || gg != 0.0)) {
-            atomicAdd(ea.g_phong, gk);
-            atomicAdd(ea.g_phong + 1, gg);
-        }
-    }
+    if (sc.target >= 0) cta_add2<kWF>(gk, gg, ea.g_phong);
 }
 
 // ------------------------------------------------------------------ K5b, lockstep packets
@@ -849,15 +858,8 @@ __global__ void __launch_bounds__(kGradTPB, M == 2 ? PRC_GRAD2_MINB : (M == 3 ? 
         own[vt.iv[i]] = own_acc[r];
         if (single && acc[r] != 0.0) atomicAdd(ea.g_vert + vt.vox[i], acc[r]);
     }
-    if (sc.target >= 0) {
-        for (int o = 16; o > 0; o >>= 1) {
-            gk += __shfl_down_sync(0xffffffffu, gk, o);
-            gg += __shfl_down_sync(0xffffffffu, gg, o);
-        }
-        if ((threadIdx.x & 31) == 0 && (gk != 0.0 || gg != 0.0)) {
-            atomicAdd(ea.g_phong, gk);
-            atomicAdd(ea.g_phong + 1, gg);
-        }
+    if constexpr (F == 0) {  // F != 0: scenes without surfaces (launch_le_gradient)
+        if (sc.target >= 0) cta_add2<kGradTPB>(gk, gg, ea.g_phong);
     }
 }
 
@@ -897,7 +899,8 @@ __global__ void PRC_PATHG_LB k_path_gradient(const __grid_constant__ DScene sc,
             any |= o != 0.0;
         }
     }
-    V3 xprev = any ? mk(st.px[rb], st.py[rb], st.pz[rb]) : mk(0, 0, 0);
+    const bool walk = ea.do_beta;  // segment spans only with a beta gradient: positions needed
+    V3 xprev = any && walk ? mk(st.px[rb], st.py[rb], st.pz[rb]) : mk(0, 0, 0);
     int b = 1;
     bool done = !any;
     double prefix = 0.0, cf = 0.0, gk = 0.0, gg = 0.0;
@@ -919,15 +922,19 @@ __global__ void PRC_PATHG_LB k_path_gradient(const __grid_constant__ DScene sc,
                 const uint32_t m = st.meta[r];
                 const uint32_t kind = meta_kind(m);
                 if (kind == VK_VOLUME && ea.do_beta) vertex_scores(sc, ea, st.vox[r], st.ct[r], after);
-                if (sc.target >= 0 && kind == VK_SURFACE && meta_surface(m) == sc.target)
-                    phong_scores(ea.phong, st.ct[r], after, gk, gg);
+                if (sc.target >= 0 && kind == VK_SURFACE && meta_surface(m) == sc.target) {
+                    if (ea.vlobe)
+                        phong_scores_lc(ea.phong, ea.vlobe[ib + (unsigned long long)(b - 1) * rs], after, gk, gg);
+                    else
+                        phong_scores(ea.phong, st.ct[r], after, gk, gg);
+                }
             }
             if (from_here != 0.0 && ea.do_beta) {
                 S.init<PAD>(sc, xprev, mk(st.dx[r], st.dy[r], st.dz[r]), st.tt[r]);
                 cf = -from_here;
             }
             prefix = prefix_next;
-            xprev = mk(st.px[r], st.py[r], st.pz[r]);
+            if (walk) xprev = mk(st.px[r], st.py[r], st.pz[r]);
             ++b;
         }
         const int walking = warp_count(S.alive);
@@ -942,16 +949,7 @@ __global__ void PRC_PATHG_LB k_path_gradient(const __grid_constant__ DScene sc,
             }
         } while (warp_count(S.alive) >= target && target > 0);
     }
-    if (sc.target >= 0) {
-        for (int o = 16; o > 0; o >>= 1) {
-            gk += __shfl_down_sync(0xffffffffu, gk, o);
-            gg += __shfl_down_sync(0xffffffffu, gg, o);
-        }
-        if ((threadIdx.x & 31) == 0 && (gk != 0.0 || gg != 0.0)) {
-            atomicAdd(ea.g_phong, gk);
-            atomicAdd(ea.g_phong + 1, gg);
-        }
-    }
+    if (sc.target >= 0) cta_add2<kTPB>(gk, gg, ea.g_phong);
 }
 
 // ------------------------------------------------------------------ padded layout
@@ -976,6 +974,205 @@ __global__ void k_unpad_add(const __grid_constant__ DScene sc, const double* __r
     double acc = g_pad[pv];
     for (int r = 1; r < copies; ++r) acc += g_pad[(long long)r * stride + pv];
     g_span[v] += acc;
+}
+
+// ------------------------------------------------------------------ event list (no medium)
+// Scenes without a medium have only surface interaction vertices and no LE walks; K4b over
+// the dense [det][i] cache is then bound by the latency of one cache load per (vertex,
+// camera) slot, most of which hold no event (config (d): 14%).  The event list keeps the
+// events only (prc_kernels.cuh, EventList).
+__global__ void k_evc_count(const __grid_constant__ DScene sc, const __grid_constant__ VertexTable vt,
+                            unsigned long long* __restrict__ cnt) {
+    const unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= vt.n) return;
+    if (meta_kind(vt.meta[i]) != VK_SURFACE) return;
+    unsigned c = 0;
+    for (int k = 0; k < sc.n_det; ++k) c += vt.ev_pix[(unsigned long long)k * vt.n + i] >= 0 ? 1u : 0u;
+    cnt[vt.iv[i]] = c;
+}
+
+__global__ void k_evc_fill(const __grid_constant__ DScene sc, const __grid_constant__ VertexTable vt,
+                           const unsigned long long* __restrict__ off, uint32_t* __restrict__ ev_iv,
+                           int32_t* __restrict__ ev_px, double* __restrict__ ev_lobe, float* __restrict__ ev_geom,
+                           uint8_t* __restrict__ ev_surf) {
+    const unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= vt.n) return;
+    const uint32_t m = vt.meta[i];
+    if (meta_kind(m) != VK_SURFACE) return;
+    const uint32_t iv = vt.iv[i];
+    unsigned long long o = off[iv];
+    const double* cosv = ev_cos_of(sc, vt);
+    const int sf = meta_surface(m);
+    const DSurf& f = sc.surf[sf];
+    for (int k = 0; k < sc.n_det; ++k) {
+        const unsigned long long e = (unsigned long long)k * vt.n + i;
+        const int pix = vt.ev_pix[e];
+        if (pix < 0) continue;
+        ev_iv[o] = iv;
+        ev_px[o] = (int32_t)(sc.det[k].img_off + pix);
+        ev_lobe[o] = sf == sc.target ? log(clampd(cosv[e], 0.0, 1.0))
+                              : brdf_eval(f.brdf_kind, f.albedo, f.kappa, f.gamma, cosv[e]);
+        ev_geom[o] = __int_as_float(vt.ev_c1[e]);
+        ev_surf[o] = (uint8_t)sf;
+        ++o;
+    }
+}
+
+// EvalArgs::vlobe (thread per path): the continuation lobe term of every surface vertex,
+// computed as K4a / K5a compute it.
+__global__ void k_vlobe(const __grid_constant__ DScene sc, const __grid_constant__ StoreView st,
+                        double* __restrict__ vlobe) {
+    const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= (long long)st.n) return;
+    const int B = (int)st.B[p];
+    const unsigned long long rb = st.rec_base[p], ib = st.iv_base[p];
+    const unsigned rs = st.stride[p];
+    for (int b = 1; b < B; ++b) {
+        const unsigned long long r = rb + (unsigned long long)b * rs;
+        const unsigned long long iv = ib + (unsigned long long)(b - 1) * rs;
+        const uint32_t m = st.meta[r];
+        double v = 0.0;
+        if (meta_kind(m) == VK_SURFACE) {
+            const int sf = meta_surface(m);
+            const double ct = st.ct[r];
+            if (sf == sc.target) {
+                v = log(clampd(ct, 0.0, 1.0));
+            } else {
+                const DSurf& f = sc.surf[sf];
+                const double fr = brdf_eval(f.brdf_kind, f.albedo, f.kappa, f.gamma, ct);
+                v = fr <= 0.0 ? -INFINITY : log(PRC_PI * fr);
+            }
+        }
+        vlobe[iv] = v;
+    }
+}
+
+// K4b' and K5b' take kEvcEPT events per thread, kEvcTPB apart, and issue all their loads
+// before the first use: a single event per thread keeps too few bytes in flight to cover
+// the two dependent round trips (event -> lp[iv]) at the HBM rate.
+constexpr int kEvcTPB = 256;
+constexpr int kEvcEPT = 4;
+
+// K4b' (thread per event): k_le_forward<true>'s cached surface event without a medium,
+// the same operations on the same values (pathstore.cpp:133-166).
+__global__ void __launch_bounds__(kEvcTPB) k_evc_forward(const __grid_constant__ DScene sc,
+                                                         const __grid_constant__ EventList el,
+                                                         const __grid_constant__ EvalArgs ea,
+                                                         const double* __restrict__ lp) {
+    const unsigned long long base = (unsigned long long)blockIdx.x * (kEvcTPB * kEvcEPT) + threadIdx.x;
+    uint32_t iv[kEvcEPT];
+    int px[kEvcEPT], sf[kEvcEPT];
+    double lobe[kEvcEPT], lpv[kEvcEPT];
+    float geom[kEvcEPT];
+#pragma unroll
+    for (int k = 0; k < kEvcEPT; ++k) {
+        const unsigned long long j = base + (unsigned long long)k * kEvcTPB;
+        iv[k] = 0xffffffffu;
+        px[k] = sf[k] = 0;
+        lobe[k] = 0.0;
+        geom[k] = 0.0f;
+        if (j < el.n) {
+            iv[k] = el.iv[j];
+            px[k] = el.px[j];
+            sf[k] = el.surf[j];
+            lobe[k] = el.lobe[j];
+            geom[k] = el.geom[j];
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < kEvcEPT; ++k) {
+        PRC_CHECK(sc, iv[k] == 0xffffffffu || iv[k] < el.n_iv, CHK_SLOT);
+        lpv[k] = iv[k] != 0xffffffffu ? lp[iv[k]] : -INFINITY;
+    }
+    unsigned clamps = 0;
+    const double kap = ea.phong[0], gam = ea.phong[1];
+#pragma unroll
+    for (int k = 0; k < kEvcEPT; ++k) {
+        const unsigned long long j = base + (unsigned long long)k * kEvcTPB;
+        if (j >= el.n) break;
+        float val = 0.0f;
+        if (lpv[k] != -INFINITY) {
+            // surf_brdf from the cached lobe term: the same operations on the same values
+            const double fr = sf[k] == sc.target ? 1.0 - kap + kap * pow01(lobe[k], gam) : lobe[k];
+            if (fr > 0.0) {
+                PRC_CHECK(sc, px[k] >= 0 && px[k] < sc.n_pix, CHK_PIXEL);
+                const double elp = fabs(lpv[k]) < 300.0 ? exp(lpv[k]) : 0.0;
+                double contrib;
+                if (elp != 0.0 && fr >= 1e-100 && fr <= 1e100) {
+                    const double direct = elp * fr;
+                    contrib = direct * (double)geom[k] * sc.prefactor;
+                } else {
+                    double logval = lpv[k] + log(fr);
+                    if (logval > PRC_LOG_CLAMP || logval < -PRC_LOG_CLAMP) {
+                        logval = clampd(logval, -PRC_LOG_CLAMP, PRC_LOG_CLAMP);
+                        ++clamps;
+                    }
+                    contrib = exp(logval) * (double)geom[k] * sc.prefactor;
+                }
+                val = (float)contrib;
+                if (contrib != 0.0) image_add(sc, ea, px[k], contrib);
+            }
+        }
+        el.val[j] = val;
+    }
+    for (int o = 16; o > 0; o >>= 1) clamps += __shfl_down_sync(0xffffffffu, clamps, o);
+    if ((threadIdx.x & 31) == 0 && clamps) atomicAdd(ea.clamps, (unsigned long long)clamps);
+}
+
+// K5b' (thread per event): w = value * residual (pathstore.cpp:196-212; no medium, so no
+// LE spans), the target surface's Phong scores, and the per-vertex weight sums own[iv]
+// (own zeroed by the caller) by a segmented warp scan over the iv-ordered events: a
+// vertex's events are contiguous, so at most two partial sums (a warp boundary) reach
+// own[iv], and 0 + a + b is order-free.  The Phong scores leave with one reduction per CTA.
+__global__ void __launch_bounds__(kEvcTPB) k_evc_gradient(const __grid_constant__ DScene sc,
+                                                          const __grid_constant__ EventList el,
+                                                          const __grid_constant__ EvalArgs ea,
+                                                          double* __restrict__ own) {
+    const int lane = threadIdx.x & 31;
+    const unsigned long long base = (unsigned long long)blockIdx.x * (kEvcTPB * kEvcEPT) + threadIdx.x;
+    uint32_t iv[kEvcEPT];
+    int px[kEvcEPT];
+    bool tg[kEvcEPT];
+    double val[kEvcEPT], wt[kEvcEPT];
+#pragma unroll
+    for (int k = 0; k < kEvcEPT; ++k) {
+        const unsigned long long j = base + (unsigned long long)k * kEvcTPB;
+        iv[k] = 0xffffffffu;
+        px[k] = 0;
+        tg[k] = false;
+        val[k] = 0.0;
+        if (j < el.n) {
+            iv[k] = el.iv[j];
+            px[k] = el.px[j];
+            tg[k] = sc.target >= 0 && el.surf[j] == sc.target;
+            val[k] = (double)el.val[j];
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < kEvcEPT; ++k) {
+        PRC_CHECK(sc, iv[k] == 0xffffffffu || (px[k] >= 0 && px[k] < sc.n_pix), CHK_PIXEL);
+        wt[k] = ea.weights && iv[k] != 0xffffffffu ? ea.weights[px[k]] : 1.0;
+    }
+    double gk = 0.0, gg = 0.0;
+#pragma unroll
+    for (int k = 0; k < kEvcEPT; ++k) {
+        const unsigned long long j = base + (unsigned long long)k * kEvcTPB;
+        const double w = ea.weights ? val[k] * wt[k] : val[k];
+        if (tg[k] && w != 0.0) phong_scores_lc(ea.phong, el.lobe[j], w, gk, gg);
+        double sum = w;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const double o = __shfl_up_sync(0xffffffffu, sum, d);
+            const uint32_t oiv = __shfl_up_sync(0xffffffffu, iv[k], d);
+            if (lane >= d && oiv == iv[k]) sum += o;
+        }
+        const uint32_t niv = __shfl_down_sync(0xffffffffu, iv[k], 1);
+        if (iv[k] != 0xffffffffu && (lane == 31 || niv != iv[k]) && sum != 0.0) {
+            PRC_CHECK(sc, iv[k] < el.n_iv, CHK_SLOT);
+            atomicAdd(own + iv[k], sum);
+        }
+    }
+    if (sc.target >= 0) cta_add2<kEvcTPB>(gk, gg, ea.g_phong);
 }
 
 }  // namespace
@@ -1065,6 +1262,45 @@ cudaError_t launch_le_gradient(const DScene& sc, const VertexTable& vt, const Ev
         LAUNCH_DONE();
     }
     k_le_gradient<<<grid_for((long long)vt.n, kWF), kWF, 0, s>>>(sc, vt, ea, own, spread);
+    LAUNCH_DONE();
+}
+
+cudaError_t launch_evc_count(const DScene& sc, const VertexTable& vt, unsigned long long* cnt, cudaStream_t s,
+                             unsigned long long* launches) {
+    if (vt.n == 0) return cudaSuccess;
+    k_evc_count<<<grid_for((long long)vt.n, 256), 256, 0, s>>>(sc, vt, cnt);
+    LAUNCH_DONE();
+}
+
+cudaError_t launch_evc_fill(const DScene& sc, const VertexTable& vt, const unsigned long long* off, uint32_t* iv,
+                            int32_t* px, double* lobe, float* geom, uint8_t* surf, cudaStream_t s,
+                            unsigned long long* launches) {
+    if (vt.n == 0) return cudaSuccess;
+    k_evc_fill<<<grid_for((long long)vt.n, 256), 256, 0, s>>>(sc, vt, off, iv, px, lobe, geom, surf);
+    LAUNCH_DONE();
+}
+
+cudaError_t launch_vlobe(const DScene& sc, const StoreView& st, double* vlobe, cudaStream_t s,
+                         unsigned long long* launches) {
+    if (st.n == 0) return cudaSuccess;
+    k_vlobe<<<grid_for((long long)st.n, 128), 128, 0, s>>>(sc, st, vlobe);
+    LAUNCH_DONE();
+}
+
+cudaError_t launch_evc_forward(const DScene& sc, const EventList& el, const EvalArgs& ea, const double* lp,
+                               cudaStream_t s, unsigned long long* launches) {
+    if (el.n == 0) return cudaSuccess;
+    k_evc_forward<<<grid_for((long long)el.n, kEvcTPB * kEvcEPT), kEvcTPB, 0, s>>>(sc, el, ea, lp);
+    LAUNCH_DONE();
+}
+
+cudaError_t launch_evc_gradient(const DScene& sc, const EventList& el, const EvalArgs& ea, double* own,
+                                cudaStream_t s, unsigned long long* launches) {
+    if (el.n_iv == 0) return cudaSuccess;
+    cudaError_t e = cudaMemsetAsync(own, 0, el.n_iv * sizeof(double), s);
+    if (e != cudaSuccess) return e;
+    if (el.n == 0) return cudaSuccess;
+    k_evc_gradient<<<grid_for((long long)el.n, kEvcTPB * kEvcEPT), kEvcTPB, 0, s>>>(sc, el, ea, own);
     LAUNCH_DONE();
 }
 

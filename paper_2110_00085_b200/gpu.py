@@ -295,7 +295,9 @@ class Context:
 
     def set_option(self, key: str, value: int):
         """'mode': 0 event-major wavefront (default) / 1 fused thread-per-path;
-        'packet': LE rays per thread in the gradient kernel (1..4, default 3); 'spread'."""
+        'packet': LE rays per thread in the gradient kernel (1..4, default 3); 'spread';
+        'events': compact event list for scenes without a medium (default 1); see
+        include/pathrec_gpu.h for the rest."""
         _check(_lib.prc_gpu_ctx_set_option(self.ptr, key.encode(), int(value)))
 
     # ------------------------------------------------------------------ scene

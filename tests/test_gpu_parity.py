@@ -816,3 +816,45 @@ def test_concurrent_calls_on_one_context_are_serialised(ctx, golden_dir):
     for (k, it), r in out.items():
         assert img_err(r.images, want[k % 2].images) <= 1e-12
         assert grad_err(r.grad_beta, want[k % 2].grad_beta) <= 1e-12
+
+
+@pytest.mark.parametrize("name", ["phong", "reflectometry"])
+def test_event_list_equals_dense_cache(ctx, golden_dir, name):
+    """Scenes without a medium evaluate over the compact event list (K4b' / K5b') once the
+    first forward over a store has written the dense event cache.  Event values are the
+    same expression in the same order, so deterministic images are bit-identical to the
+    dense kernels' and the Phong gradient differs only in the order of its sums; the list
+    is rebuilt after a re-sort (new vertex-table order) and after a camera change."""
+    if name == "phong":
+        scene = FIXTURES["phong"]["scene"]()
+    else:
+        scene = S.reflectometry_scene(24, 24, 6)
+    w = np.linspace(-1.0, 1.0, scene.pixel_count)
+    p = perturbed(scene)
+    opts = EvalOptions(want_grad=True, pixel_weights=w, deterministic=True)
+    out = {}
+    for ev in (0, 1):
+        ctx.set_option("events", ev)
+        ctx.upload(scene)
+        if name == "phong":
+            st = ctx.load_store(str(golden_dir / "phong.pstr"))
+        else:
+            st = ctx.render(scene, RenderOptions(n_paths=20000, seed=11, keep_paths=True)).store
+        runs = [ctx.evaluate_store(scene, st, p, opts) for _ in range(3)]
+        ctx.sort_by_size(st)
+        runs += [ctx.evaluate_store(scene, st, p, opts) for _ in range(2)]
+        st.free()
+        out[ev] = runs
+    ctx.set_option("events", 1)
+    ref = out[0][0]
+    assert ref.images.max() > 0.0
+    for r in out[0] + out[1]:
+        assert np.array_equal(r.images, ref.images)
+        assert r.clamp_events == ref.clamp_events
+        assert scalar_err(r.grad_kappa, ref.grad_kappa) <= 1e-12
+        assert scalar_err(r.grad_gamma, ref.grad_gamma) <= 1e-12
+    if name == "phong":
+        g = golden("phong")
+        r = ctx.evaluate_store(scene, ctx.load_store(str(golden_dir / "phong.pstr")), p,
+                               EvalOptions(want_grad=True, pixel_weights=weight_patterns(scene)["w"]))
+        assert img_err(r.images, g["pert_w_images"]) <= IMG_TOL
