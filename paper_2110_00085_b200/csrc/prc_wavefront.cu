@@ -863,6 +863,48 @@ __global__ void __launch_bounds__(kGradTPB, M == 2 ? PRC_GRAD2_MINB : (M == 3 ? 
     }
 }
 
+// K5a without a beta gradient (no medium, or no unknown species and no per-type
+// gradients): of pathstore.cpp:213-237 only the target surface's continuation Phong
+// scores remain -- no spans to scatter, so no regeneration and none of k_path_gradient's
+// walk state.  The same arithmetic in the same order as k_path_gradient.
+__global__ void __launch_bounds__(kTPB) k_path_scores(const __grid_constant__ DScene sc,
+                                                      const __grid_constant__ StoreView st,
+                                                      const __grid_constant__ EvalArgs ea,
+                                                      const double* __restrict__ own) {
+    const long long p = path_index(st.n);
+    const int B = p >= 0 ? (int)st.B[p] : 0;
+    double gk = 0.0, gg = 0.0;
+    if (B >= 2) {
+        const unsigned long long rb = st.rec_base[p], ib = st.iv_base[p];
+        const unsigned rs = st.stride[p];
+        double W = 0.0;
+        bool any = false;
+        for (int b = 1; b < B; ++b) {
+            const double o = own[ib + (unsigned long long)(b - 1) * rs];
+            W += o;
+            any |= o != 0.0;
+        }
+        double prefix = 0.0;
+        for (int b = 1; b < B && any; ++b) {
+            const unsigned long long iv = ib + (unsigned long long)(b - 1) * rs;
+            const double prefix_next = prefix + own[iv];
+            const double after = W - prefix_next;
+            if (after != 0.0) {
+                const unsigned long long r = rb + (unsigned long long)b * rs;
+                const uint32_t m = st.meta[r];
+                if (meta_kind(m) == VK_SURFACE && meta_surface(m) == sc.target) {
+                    if (ea.vlobe)
+                        phong_scores_lc(ea.phong, ea.vlobe[iv], after, gk, gg);
+                    else
+                        phong_scores(ea.phong, st.ct[r], after, gk, gg);
+                }
+            }
+            prefix = prefix_next;
+        }
+    }
+    cta_add2<kTPB>(gk, gg, ea.g_phong);
+}
+
 // ------------------------------------------------------------------ K5a path suffix
 // Thread per path (B-sorted).  Segment lengths (in voxels) are exponentially distributed,
 // so a warp walking "segment b of every lane" in lockstep idles most lanes.  Instead every
@@ -1129,7 +1171,10 @@ __global__ void __launch_bounds__(kEvcTPB) k_evc_gradient(const __grid_constant_
                                                           const __grid_constant__ EvalArgs ea,
                                                           double* __restrict__ own) {
     const int lane = threadIdx.x & 31;
-    const unsigned long long base = (unsigned long long)blockIdx.x * (kEvcTPB * kEvcEPT) + threadIdx.x;
+    double gk = 0.0, gg = 0.0;
+    for (unsigned long long c0 = (unsigned long long)blockIdx.x * (kEvcTPB * kEvcEPT); c0 < el.n;
+         c0 += (unsigned long long)gridDim.x * (kEvcTPB * kEvcEPT)) {
+    const unsigned long long base = c0 + threadIdx.x;
     uint32_t iv[kEvcEPT];
     int px[kEvcEPT];
     bool tg[kEvcEPT];
@@ -1153,7 +1198,6 @@ __global__ void __launch_bounds__(kEvcTPB) k_evc_gradient(const __grid_constant_
         PRC_CHECK(sc, iv[k] == 0xffffffffu || (px[k] >= 0 && px[k] < sc.n_pix), CHK_PIXEL);
         wt[k] = ea.weights && iv[k] != 0xffffffffu ? ea.weights[px[k]] : 1.0;
     }
-    double gk = 0.0, gg = 0.0;
 #pragma unroll
     for (int k = 0; k < kEvcEPT; ++k) {
         const unsigned long long j = base + (unsigned long long)k * kEvcTPB;
@@ -1171,6 +1215,7 @@ __global__ void __launch_bounds__(kEvcTPB) k_evc_gradient(const __grid_constant_
             PRC_CHECK(sc, iv[k] < el.n_iv, CHK_SLOT);
             atomicAdd(own + iv[k], sum);
         }
+    }
     }
     if (sc.target >= 0) cta_add2<kEvcTPB>(gk, gg, ea.g_phong);
 }
@@ -1287,6 +1332,16 @@ cudaError_t launch_vlobe(const DScene& sc, const StoreView& st, double* vlobe, c
     LAUNCH_DONE();
 }
 
+// K5b' runs persistent: 4 resident CTAs per SM (56 registers) stride over the events, so
+// no CTA retires waiting for its reductions to drain (r2 at config (d): 1.55 -> 1.12 ms
+// against one CTA per 1024 events; K4b' the other way round, 1.015 vs 1.045 ms).
+unsigned evc_blocks(unsigned long long n) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return (unsigned)std::min<long long>(grid_for((long long)n, kEvcTPB * kEvcEPT), 4ll * std::max(sms, 1));
+}
+
 cudaError_t launch_evc_forward(const DScene& sc, const EventList& el, const EvalArgs& ea, const double* lp,
                                cudaStream_t s, unsigned long long* launches) {
     if (el.n == 0) return cudaSuccess;
@@ -1300,13 +1355,18 @@ cudaError_t launch_evc_gradient(const DScene& sc, const EventList& el, const Eva
     cudaError_t e = cudaMemsetAsync(own, 0, el.n_iv * sizeof(double), s);
     if (e != cudaSuccess) return e;
     if (el.n == 0) return cudaSuccess;
-    k_evc_gradient<<<grid_for((long long)el.n, kEvcTPB * kEvcEPT), kEvcTPB, 0, s>>>(sc, el, ea, own);
+    k_evc_gradient<<<evc_blocks(el.n), kEvcTPB, 0, s>>>(sc, el, ea, own);
     LAUNCH_DONE();
 }
 
 cudaError_t launch_path_gradient(const DScene& sc, const StoreView& st, const EvalArgs& ea,
                                  const double* own, cudaStream_t s, unsigned long long* launches) {
     if (st.n == 0) return cudaSuccess;
+    if (!ea.do_beta) {  // only the target surface's Phong scores
+        if (sc.target < 0) return cudaSuccess;
+        k_path_scores<<<grid_for((long long)st.n, kTPB), kTPB, 0, s>>>(sc, st, ea, own);
+        LAUNCH_DONE();
+    }
     if (sc.pad_walk)
         k_path_gradient<true><<<grid_for((long long)st.n, kTPB), kTPB, 0, s>>>(sc, st, ea, own);
     else
