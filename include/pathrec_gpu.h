@@ -171,7 +171,7 @@ int prc_gpu_ctx_rank(const prc_gpu_ctx* ctx, int* rank, int* world);
 /* Engine knobs: "mode" 0 = event-major wavefront over Morton-ordered interaction
  * vertices (default), 1 = fused thread-per-path (the paper's mapping); "packet" 1..4 =
  * LE rays per thread walked in lockstep by the gradient kernel (default 3); "spread" =
- * Morton distance between the packets of one warp (default 64); "per_species" 1 = the
+ * Morton distance between the packets of one warp (default 0: by vertex density); "per_species" 1 = the
  * device-resident iteration (prc_gpu_opt_step) computes per-type gradients of every
  * species (config (c)); the optimiser still updates the unknown species; "pad" 0 turns
  * off the guard-free walks over the padded voxel layout (default 1; same results);

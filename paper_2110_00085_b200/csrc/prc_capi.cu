@@ -111,7 +111,7 @@ struct prc_gpu_ctx {
     unsigned long long launches = 0;
     int mode = 0;        // 0: event-major wavefront (default), 1: fused thread-per-path
     bool timed_sub = false, timed_grad = false;  // sub-phase events recorded this call
-    int spread = 64;     // K5b lane spreading factor (measured at 1e8: 64-128 best; 16 +10%, 1 +25%)
+    int spread = 0;      // K5b lane spreading factor; 0: by vertex density (auto_spread)
     int opt_per_species = 0;  // opt_step computes per-type gradients of every species
     int packet = 3;      // K5b rays per thread walked in lockstep (measured best: 3)
     bool evc_enable = true;  // event list for scenes without a medium (option "events")
@@ -582,12 +582,16 @@ void upload_scene(prc_gpu_ctx* c, const prc_scene_desc* d) {
         c->db_pad.alloc(vpad);
         // copies of the padded gradient for K5b (EvalArgs::g_pad_copies): 8 while they take
         // at most 2 GB (K5b at 1e8 paths: 784 -> 697 ms with 4 copies at 128^3, 670 -> 663 with
-        // 8; 1973 -> 1728 ms with 4 at 256^3, where one copy alone exceeds L2); an explicit
+        // 8; 1973 -> 1728 ms with 4 at 256^3, where one copy alone exceeds L2), and up to 32
+        // while they fit in 64 MB of L2 (small grids, where reductions into the same lines
+        // queue: config (a), 32^3, K5b 2.42 -> 2.28 ms with 32 copies); an explicit
         // "grad_copies" option is taken as given
+        const size_t l2_copies = vpad > 0 ? (size_t(64) << 20) / (vpad * 8) : 1;
         c->g_pad_copies = !(c->pad_ok && vpad > 0) ? 1
                           : c->grad_copies_max > 0
                               ? c->grad_copies_max
-                              : (int)std::max<size_t>(1, std::min<size_t>(8, (size_t(2) << 30) / (vpad * 8)));
+                              : (int)std::max<size_t>(1, std::min<size_t>(std::max<size_t>(8, std::min<size_t>(32, l2_copies)),
+                                                                          (size_t(2) << 30) / (vpad * 8)));
         c->g_pad.alloc(vpad * (size_t)c->g_pad_copies);
         CK(cudaMemset(c->bt_pad.p, 0, c->bt_pad.bytes()));  // borders stay zero
         CK(cudaMemset(c->db_pad.p, 0, c->db_pad.bytes()));
@@ -1046,6 +1050,18 @@ void run_forward(prc_gpu_ctx* c, prc_gpu_store* st, const Resolved& r, const Eva
     CK(cudaEventRecord(c->ev[3], q));
 }
 
+// K5b lane spreading by interaction vertices per voxel d.  Round 2, K5b ms at spread
+// 4 / 16 / 32 / 64: (b) 1e8 paths at 128^3 (d = 150) 672 / 603 / 602 / 607, (c) (d = 151)
+// - / 714 / 704 / 705; 3e7 paths (d = 45) 188 / 185 / 189 / -; 1e7 paths (d = 15)
+// 64.5 / 67.3 / - / 74.0; (e) 256^3 (d = 23) 1499 / 1524 / 1584 / 1658; (a) 32^3 (d = 96,
+// 32 copies) 2.28 / 2.39 / 2.47 / 2.52.  Dense tables want lanes far apart (same-voxel
+// reductions), sparse ones want them close (coherent walks).
+int auto_spread(const prc_gpu_ctx* c, const prc_gpu_store* st) {
+    if (c->spread > 0) return c->spread;
+    const double d = (double)st->n_iv / (double)std::max<long long>(c->V, 1);
+    return d >= 120.0 ? 32 : 4;
+}
+
 // K5 gradient with weights ea.weights, then its reduction over ranks and the combination
 // grad_j = scale (g_span + g_vert[j]) (n_out species slices) into c->grad_res.  Event [4]
 // after K5.  With NVLS (option "nvls") one fold kernel does the padded-copy sum, the
@@ -1066,7 +1082,7 @@ void run_gradient(prc_gpu_ctx* c, prc_gpu_store* st, const EvalArgs& ea, int n_o
         if (evc_ready(c, st) && st->evc_vals)
             CK(launch_evc_gradient(s, event_list(st), ea, st->own.p, q, &c->launches));
         else
-            CK(launch_le_gradient(s, vertex_table(st), ea, st->own.p, ea.do_beta ? c->spread : 1,
+            CK(launch_le_gradient(s, vertex_table(st), ea, st->own.p, ea.do_beta ? auto_spread(c, st) : 1,
                                   s.pad_walk ? c->packet : 1, q, &c->launches));
         CK(cudaEventRecord(c->ev[7], q));
         c->timed_grad = true;
@@ -1930,8 +1946,8 @@ PRC_EXPORT int prc_gpu_ctx_set_option(prc_gpu_ctx* ctx, const char* key, int64_t
     if (k == "mode") {
         if (value != 0 && value != 1) return fail(PRC_ERR_CONFIG, "mode must be 0 (wavefront) or 1 (path)");
         ctx->mode = (int)value;
-    } else if (k == "spread") {
-        if (value < 1 || value > 4096) return fail(PRC_ERR_CONFIG, "spread must be in 1..4096");
+    } else if (k == "spread") {  // 0: by vertex density
+        if (value < 0 || value > 4096) return fail(PRC_ERR_CONFIG, "spread must be in 0..4096");
         ctx->spread = (int)value;
     } else if (k == "per_species") {
         ctx->opt_per_species = value ? 1 : 0;
