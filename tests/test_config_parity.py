@@ -127,6 +127,40 @@ def test_reference_written_config_a_store(ctx, ref, tmp_path):
     assert e_img <= IMG_TOL and e_grad <= GRAD_TOL
 
 
+def test_config_d_store_matches_reference(ctx, ref, tmp_path):
+    """Config (d), reflectometry (phong_box walls, the central Phong sphere as the unknown,
+    14 diffuse spheres, 16 inward cameras at 256^2): no medium, so after the first forward
+    over the store the device evaluates its compact event list (K4b' / K5b', cached lobe
+    terms, K5a reduced to the Phong scores).  A device-traced store, exported to PSTR v1,
+    evaluated by the reference at the recycle point (kappa, gamma) = (0.55, 38): images and
+    d kappa, d gamma within 1e-5, through both the dense first pass and the event list."""
+    scene = S.reflectometry_scene(256, 256, 16)
+    ctx.upload(scene)
+    rr = ctx.render(scene, RenderOptions(n_paths=20_000, seed=7, keep_paths=True))
+    st = rr.store
+    ctx.sort_by_size(st)
+    pstr = str(tmp_path / "d.pstr")
+    st.save(pstr)
+    t = S.ParamSet(None, 0.55, 38.0)
+    F_ref = ref.evaluate(scene, pstr, None, abi.PRC_EVAL_NORMALIZE, workers=WORKERS)["images"]
+    F_t = ref.evaluate(scene, pstr, t, abi.PRC_EVAL_NORMALIZE, workers=WORKERS)["images"]
+    w = F_t - 0.9 * F_ref
+    r = ref.evaluate(scene, pstr, t, abi.PRC_EVAL_NORMALIZE | abi.PRC_EVAL_WANT_GRAD, w, workers=WORKERS)
+    e_ref = img_err(ctx.recycled_render(scene, st, None), F_ref)  # dense pass, builds the list
+    msg = [f"config (d) 20000 paths: F_ref {e_ref:.2e}"]
+    for k in range(2):  # event list
+        g = ctx.evaluate_store(scene, st, t, EvalOptions(want_grad=True, pixel_weights=w))
+        e_img = img_err(g.images, r["images"])
+        e_k = abs(g.grad_kappa - r["grad_kappa"]) / max(abs(r["grad_kappa"]), 1e-300)
+        e_g = abs(g.grad_gamma - r["grad_gamma"]) / max(abs(r["grad_gamma"]), 1e-300)
+        msg.append(f"F_t {e_img:.2e}, d kappa {e_k:.2e}, d gamma {e_g:.2e}")
+        assert g.clamp_events == r["clamp_events"]
+        assert e_ref <= IMG_TOL and e_img <= IMG_TOL and e_k <= GRAD_TOL and e_g <= GRAD_TOL, msg
+    assert r["images"].max() > 0.0 and r["grad_kappa"] != 0.0
+    print("; ".join(msg))
+    st.free()
+
+
 def test_full_size_order_and_mapping_invariance(ctx):
     """Config (b) at the bench's 1e8 paths: the recycled image and gradient do not depend
     on the storage order (path-major trace order vs sorted by B, sort invariance of
