@@ -646,6 +646,16 @@ __global__ void __launch_bounds__(kGradTPB, M == 2 ? PRC_GRAD2_MINB : (M == 3 ? 
     double own_acc[M], acc[M];
 #pragma unroll
     for (int r = 0; r < M; ++r) own_acc[r] = acc[r] = 0.0;
+    // F = 2 with per-type gradients: each packet slot's per-species vertex scores summed over
+    // the cameras in shared memory (thread-private rows), one reduction per (vertex,
+    // species) after the camera loop instead of one per event (config (c))
+    double* accj = nullptr;
+    if constexpr (F == 2) {
+        __shared__ double s_accj[kGradTPB * M * kFCacheMax];
+        accj = s_accj + threadIdx.x * (M * kFCacheMax);
+#pragma unroll
+        for (int q = 0; q < M * kFCacheMax; ++q) accj[q] = 0.0;
+    }
     double gk = 0.0, gg = 0.0;
     for (int k = 0; k < sc.n_det; ++k) {
         DdaState S[M];
@@ -686,7 +696,7 @@ __global__ void __launch_bounds__(kGradTPB, M == 2 ? PRC_GRAD2_MINB : (M == 3 ? 
                             acc[r] += w * (sc.sp[sc.unknown].albedo * (double)fj[sc.unknown] / num);
                         else
                             for (int j = 0; j < sc.n_species; ++j)
-                                atomicAdd(ea.g_vert + (long long)j * sc.V + vox, w * (sc.sp[j].albedo * (double)fj[j] / num));
+                                accj[r * kFCacheMax + j] += w * (sc.sp[j].albedo * (double)fj[j] / num);
                     }
                 }
                 continue;
@@ -857,6 +867,15 @@ __global__ void __launch_bounds__(kGradTPB, M == 2 ? PRC_GRAD2_MINB : (M == 3 ? 
         if (pk >= n_pk || i >= vt.n) continue;
         own[vt.iv[i]] = own_acc[r];
         if (single && acc[r] != 0.0) atomicAdd(ea.g_vert + vt.vox[i], acc[r]);
+        if constexpr (F == 2) {
+            if (!single) {
+                const int vox = vt.vox[i];
+                for (int j = 0; j < sc.n_species; ++j) {
+                    const double a = accj[r * kFCacheMax + j];
+                    if (a != 0.0) atomicAdd(ea.g_vert + (long long)j * sc.V + vox, a);
+                }
+            }
+        }
     }
     if constexpr (F == 0) {  // F != 0: scenes without surfaces (launch_le_gradient)
         if (sc.target >= 0) cta_add2<kGradTPB>(gk, gg, ea.g_phong);
