@@ -190,9 +190,12 @@ def run_ours(args):
         ctx.set_option("grad_copies", args.grad_copies)
     ctx.upload(scene)
     tp = t_params(scene)
-    # warm-up resample on a small store: loads every kernel module (CUDA lazy loading) and
-    # sizes the context's scratch, so the timed resample below is a steady-state one
-    warm = ctx.render(scene, RenderOptions(n_paths=min(n_paths, 50_000), seed=1, keep_paths=True,
+    # warm-up resample at the full store size (another seed): loads every kernel module (CUDA
+    # lazy loading), sizes the context's scratch and maps the store's memory once, so the
+    # timed resample below is a steady-state one of the loop (inverse.cpp:175-204 frees the
+    # previous generation and traces the next every recycle_period iterations); first-touch
+    # allocations otherwise vary by 10x with what ran on the box before
+    warm = ctx.render(scene, RenderOptions(n_paths=n_paths, seed=1, keep_paths=True,
                                            max_bounces=max_bounces(cfg), images=False)).store
     ctx.sort_by_size(warm)
     ctx.opt_init(tp, np.zeros(scene.pixel_count), alpha=1e-3)

