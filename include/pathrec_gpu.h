@@ -166,8 +166,17 @@ int prc_gpu_ctx_create_rank(int device, int rank, int world, const void* nccl_id
 /* The contiguous stream range [lo, hi) rank `rank` of `world` owns out of n paths
  * (floor(n r / w) .. floor(n (r+1) / w)).  Host-only, no device needed. */
 int prc_gpu_shard_range(uint64_t n, int rank, int world, uint64_t* lo, uint64_t* hi);
+/* Destroys the context (its stores stay freeable) and returns the device's cached blocks. */
 void prc_gpu_ctx_destroy(prc_gpu_ctx* ctx);
 int prc_gpu_ctx_rank(const prc_gpu_ctx* ctx, int* rank, int* world);
+/* Device memory: freed buffers of >= 1 MB (a freed store's arrays, scratch) are kept by the
+ * engine and reused by later allocations of nearly the same size -- the resample of the
+ * recycling loop frees one path-store generation and allocates the next -- instead of
+ * being returned to the driver.  They are returned when a context on that device is
+ * destroyed, when an engine allocation fails, or by this call (every device).  A caller
+ * that shares the GPU with another allocator (e.g. torch) can call it after freeing
+ * stores. */
+int prc_gpu_release_cached_memory(void);
 /* Engine knobs: "mode" 0 = event-major wavefront over Morton-ordered interaction
  * vertices (default), 1 = fused thread-per-path (the paper's mapping); "packet" 1..4 =
  * LE rays per thread walked in lockstep by the gradient kernel (default 3); "spread" =

@@ -2070,6 +2070,11 @@ PRC_EXPORT int prc_gpu_ctx_set_option(prc_gpu_ctx* ctx, const char* key, int64_t
     return PRC_OK;
 }
 
+PRC_EXPORT int prc_gpu_release_cached_memory(void) {
+    cache_release(-1);
+    return PRC_OK;
+}
+
 PRC_EXPORT int prc_gpu_ctx_rank(const prc_gpu_ctx* ctx, int* rank, int* world) {
     if (!ctx || !rank || !world) return fail(PRC_ERR_INVALID, "prc_gpu_ctx_rank: null argument");
     *rank = ctx->rank;

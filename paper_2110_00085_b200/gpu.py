@@ -87,6 +87,7 @@ def load_library(path: Optional[str] = None):
         "prc_gpu_shard_range": [C.c_uint64, C.c_int, C.c_int, _u64p, _u64p],
         "prc_gpu_ctx_destroy": [vp],
         "prc_gpu_ctx_rank": [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)],
+        "prc_gpu_release_cached_memory": [],
         "prc_gpu_ctx_set_option": [vp, C.c_char_p, C.c_int64],
         "prc_gpu_scene_upload": [vp, vp],
         "prc_gpu_scene_voxel_count": [vp, _u64p],
@@ -525,6 +526,11 @@ class Context:
         _check(_lib.prc_gpu_debug_pixel_of(self.ptr, det, pts.shape[0], _ptr(pts, _dp),
                                            _ptr(out, _i32p)))
         return out
+
+
+def release_cached_memory():
+    """Returns the engine's cached device blocks (freed stores' arrays) to the driver."""
+    _check(load_library().prc_gpu_release_cached_memory())
 
 
 def metrics(estimate: np.ndarray, truth: np.ndarray):

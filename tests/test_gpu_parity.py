@@ -862,3 +862,31 @@ def test_event_list_equals_dense_cache(ctx, golden_dir, name):
         r = ctx.evaluate_store(scene, ctx.load_store(str(golden_dir / "phong.pstr")), p,
                                EvalOptions(want_grad=True, pixel_weights=weight_patterns(scene)["w"]))
         assert img_err(r.images, g["pert_w_images"]) <= IMG_TOL
+
+
+def test_block_cache_reuse_across_store_generations(ctx):
+    """Freed stores' device blocks are reused by the next generation (the recycling loop's
+    resample); a store on reused blocks evaluates exactly like one on fresh memory, and
+    the cache can be handed back to the driver."""
+    from paper_2110_00085_b200 import gpu
+    from paper_2110_00085_b200.gpu import Context
+    s = S.cloud_scene(16, 12, 12)
+    ctx.upload(s)
+    t = S.ParamSet(S.recycle_point(s.species[0].extinction))
+    opt = EvalOptions(want_grad=True, deterministic=True)
+    for seed in (5, 6):  # generation 2 lands on generation 1's blocks
+        st = ctx.render(s, RenderOptions(n_paths=200_000, seed=seed, keep_paths=True)).store
+        ctx.sort_by_size(st)
+        got = ctx.evaluate_store(s, st, t, opt)
+        st.free()
+    gpu.release_cached_memory()
+    fresh = Context(0)
+    try:
+        fresh.upload(s)
+        st = fresh.render(s, RenderOptions(n_paths=200_000, seed=6, keep_paths=True)).store
+        fresh.sort_by_size(st)
+        ref = fresh.evaluate_store(s, st, t, opt)
+    finally:
+        fresh.close()
+    assert np.array_equal(got.images, ref.images)
+    assert grad_err(got.grad_beta, ref.grad_beta) <= 1e-12
