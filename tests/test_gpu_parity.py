@@ -892,3 +892,22 @@ def test_block_cache_reuse_across_store_generations(ctx):
         fresh.close()
     assert np.array_equal(got.images, ref.images)
     assert grad_err(got.grad_beta, ref.grad_beta) <= 1e-12
+
+
+@pytest.mark.parametrize("name", ["cloud", "phong"])
+def test_ragged_store_sizes(ctx, name):
+    """Stores whose path and vertex counts are not multiples of a warp, a ray packet (3) or
+    the event list's 4 events per thread: the recycled image at the sampling point equals
+    the fresh render (pathstore.cpp:370-375 vs transport.cpp:405-454) bit for bit with
+    deterministic sums, through the cached-geometry passes as well."""
+    scene = FIXTURES[name]["scene"]()
+    ctx.upload(scene)
+    for n in (1, 2, 3, 5, 31, 33, 97, 1001):
+        rr = ctx.render(scene, RenderOptions(n_paths=n, seed=17 + n, keep_paths=True,
+                                             max_bounces=FIXTURES[name].get("max_bounces", 500)))
+        st = rr.store
+        ctx.sort_by_size(st)
+        for _ in range(2):  # the second pass reads the event caches / the event list
+            r = ctx.evaluate_store(scene, st, None, EvalOptions(deterministic=True))
+            assert np.array_equal(r.images, rr.images), (name, n)
+        st.free()
