@@ -538,12 +538,13 @@ def test_recycling_speed_benefit(ctx):
     ctx.upload(s)
     gt = ctx.render(s, RenderOptions(n_paths=1_000_000, seed=612)).images
     init = S.ParamSet(0.9 * s.species[0].extinction)
-    speed = {}
-    for nr in (30, 1):
-        t0 = time.perf_counter()
-        ctx.reconstruct(s, gt, init, n_paths=2_000_000, seed=41, recycle_period=nr, max_iterations=30,
-                        alpha=0.02)
-        speed[nr] = 30 / (time.perf_counter() - t0)
+    speed = {30: 0.0, 1: 0.0}
+    for _ in range(2):  # best of two runs each: the box's other tenants add noise
+        for nr in (30, 1):
+            t0 = time.perf_counter()
+            ctx.reconstruct(s, gt, init, n_paths=2_000_000, seed=41, recycle_period=nr, max_iterations=30,
+                            alpha=0.02)
+            speed[nr] = max(speed[nr], 30 / (time.perf_counter() - t0))
     print(f"recycling: {speed[30]:.1f} it/s with N_r = 30, {speed[1]:.1f} it/s with N_r = 1")
     assert speed[30] >= 2.0 * speed[1], speed
 
