@@ -12,8 +12,7 @@
 // vertex loop is warp-uniform and every record field is a single coalesced load.
 // Voxel spans are never stored: each pass re-walks segments and local-estimation (LE)
 // rays with the bit-exact fp64 DDA of prc_device.cuh.
-#include <cub/device/device_reduce.cuh>
-#include <cub/device/device_scan.cuh>
+#include <algorithm>
 
 #include "prc_eval.cuh"
 
@@ -26,6 +25,112 @@ constexpr int kTPB = 128;
 inline unsigned grid_for(long long n, int tpb = kTPB) {
     long long g = (n + tpb - 1) / tpb;
     return (unsigned)(g < 1 ? 1 : g);
+}
+
+// ------------------------------------------------------------------ scan / max (resample path)
+constexpr int kScanTPB = 512;
+constexpr int kScanIPT = 8;
+constexpr int kScanChunk = kScanTPB * kScanIPT;
+
+__device__ __forceinline__ unsigned long long block_sum_u64(unsigned long long v, unsigned long long* sw) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) sw[w] = v;
+    __syncthreads();
+    unsigned long long t = 0;
+    if (threadIdx.x == 0)
+        for (int i = 0; i < kScanTPB / 32; ++i) t += sw[i];
+    return t;  // valid in thread 0
+}
+
+__global__ void __launch_bounds__(kScanTPB) k_chunk_sum(const unsigned long long* __restrict__ in, long long n,
+                                                        unsigned long long* __restrict__ sums) {
+    __shared__ unsigned long long sw[kScanTPB / 32];
+    const long long base = (long long)blockIdx.x * kScanChunk;
+    unsigned long long v = 0;
+#pragma unroll
+    for (int k = 0; k < kScanIPT; ++k) {
+        const long long i = base + (long long)k * kScanTPB + threadIdx.x;
+        if (i < n) v += in[i];
+    }
+    const unsigned long long t = block_sum_u64(v, sw);
+    if (threadIdx.x == 0) sums[blockIdx.x] = t;
+}
+
+// out may alias in: a CTA reads its chunk into shared memory before writing it.
+__global__ void __launch_bounds__(kScanTPB) k_chunk_scan(const unsigned long long* in, long long n,
+                                                         const unsigned long long* __restrict__ offs,
+                                                         unsigned long long* out) {
+    __shared__ unsigned long long sm[kScanChunk];
+    __shared__ unsigned long long sw[kScanTPB / 32];
+    const long long base = (long long)blockIdx.x * kScanChunk;
+#pragma unroll
+    for (int k = 0; k < kScanIPT; ++k) {
+        const int j = k * kScanTPB + threadIdx.x;
+        const long long i = base + j;
+        sm[j] = i < n ? in[i] : 0ull;
+    }
+    __syncthreads();
+    // each thread owns kScanIPT consecutive elements
+    unsigned long long local[kScanIPT], tot = 0;
+#pragma unroll
+    for (int k = 0; k < kScanIPT; ++k) {
+        local[k] = tot;
+        tot += sm[threadIdx.x * kScanIPT + k];
+    }
+    // exclusive scan of the thread totals: warp scan, then the warp totals
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    unsigned long long inc = tot;
+    for (int d = 1; d < 32; d <<= 1) {
+        const unsigned long long o = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += o;
+    }
+    if (lane == 31) sw[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+        unsigned long long x = lane < kScanTPB / 32 ? sw[lane] : 0ull;
+        for (int d = 1; d < 32; d <<= 1) {
+            const unsigned long long o = __shfl_up_sync(0xffffffffu, x, d);
+            if (lane >= d) x += o;
+        }
+        if (lane < kScanTPB / 32) sw[lane] = x;  // inclusive warp-total prefix
+    }
+    __syncthreads();
+    const unsigned long long off = (offs ? offs[blockIdx.x] : 0ull) + (w > 0 ? sw[w - 1] : 0ull) + (inc - tot);
+#pragma unroll
+    for (int k = 0; k < kScanIPT; ++k) sm[threadIdx.x * kScanIPT + k] = off + local[k];
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kScanIPT; ++k) {
+        const int j = k * kScanTPB + threadIdx.x;
+        const long long i = base + j;
+        if (i < n) out[i] = sm[j];
+    }
+}
+
+__global__ void k_max_u32(const uint32_t* __restrict__ in, long long n, uint32_t* out) {
+    uint32_t m = 0;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        m = max(m, in[i]);
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_down_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+// exclusive scan of in[0, n) into out, chunk sums in tmp (then the next level's after them)
+cudaError_t scan_levels(const unsigned long long* in, unsigned long long* out, long long n,
+                        unsigned long long* tmp, cudaStream_t s) {
+    const long long chunks = (n + kScanChunk - 1) / kScanChunk;
+    if (chunks == 1) {
+        k_chunk_scan<<<1, kScanTPB, 0, s>>>(in, n, nullptr, out);
+        return cudaGetLastError();
+    }
+    k_chunk_sum<<<(unsigned)chunks, kScanTPB, 0, s>>>(in, n, tmp);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    e = scan_levels(tmp, tmp, chunks, tmp + chunks, s);  // chunk offsets, in place
+    if (e != cudaSuccess) return e;
+    k_chunk_scan<<<(unsigned)chunks, kScanTPB, 0, s>>>(in, n, tmp, out);
+    return cudaGetLastError();
 }
 
 // ============================================================================ K1 trace
@@ -868,14 +973,25 @@ cudaError_t launch_adam(double* x, double* m1, double* m2, const double* g, long
     LAUNCH_DONE();
 }
 
+// Exclusive u64 scan, reduce-then-scan: a CTA of kScanTPB threads owns a chunk of
+// kScanChunk elements.  Pass 1 writes the chunk sums, the chunk sums are scanned in place
+// by the same routine (one more level per 4096x), pass 2 scans each chunk in shared memory
+// from its chunk offset.  Used on the resample path (trace offsets, the sort's tile
+// histograms, the event list), 1e8-element scans take ~0.1 ms.
 cudaError_t scan_u64(const unsigned long long* in, unsigned long long* out, long long n, void** tmp,
                      size_t* tmp_bytes, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    // chunk-sum arrays of every level, in tmp
     size_t need = 0;
-    cudaError_t e = cub::DeviceScan::ExclusiveSum(nullptr, need, in, out, n, s);
-    if (e != cudaSuccess) return e;
+    for (long long m = n; m > 1;) {
+        m = (m + kScanChunk - 1) / kScanChunk;
+        need += (size_t)m * sizeof(unsigned long long);
+        if (m == 1) break;
+    }
+    need = need > 0 ? need : sizeof(unsigned long long);
     if (need > *tmp_bytes) {
         if (*tmp) cudaFree(*tmp);
-        e = cudaMalloc(tmp, need);
+        cudaError_t e = cudaMalloc(tmp, need);
         if (e != cudaSuccess) {
             *tmp = nullptr;
             *tmp_bytes = 0;
@@ -883,25 +999,18 @@ cudaError_t scan_u64(const unsigned long long* in, unsigned long long* out, long
         }
         *tmp_bytes = need;
     }
-    return cub::DeviceScan::ExclusiveSum(*tmp, need, in, out, n, s);
+    return scan_levels(in, out, n, static_cast<unsigned long long*>(*tmp), s);
 }
 
 cudaError_t reduce_max_u32(const uint32_t* in, long long n, uint32_t* out_dev, void** tmp,
                            size_t* tmp_bytes, cudaStream_t s) {
-    size_t need = 0;
-    cudaError_t e = cub::DeviceReduce::Max(nullptr, need, in, out_dev, n, s);
-    if (e != cudaSuccess) return e;
-    if (need > *tmp_bytes) {
-        if (*tmp) cudaFree(*tmp);
-        e = cudaMalloc(tmp, need);
-        if (e != cudaSuccess) {
-            *tmp = nullptr;
-            *tmp_bytes = 0;
-            return e;
-        }
-        *tmp_bytes = need;
-    }
-    return cub::DeviceReduce::Max(*tmp, need, in, out_dev, n, s);
+    (void)tmp;
+    (void)tmp_bytes;
+    cudaError_t e = cudaMemsetAsync(out_dev, 0, sizeof(uint32_t), s);
+    if (e != cudaSuccess || n <= 0) return e;
+    const long long blocks = std::min<long long>((n + 1023) / 1024, 4096);
+    k_max_u32<<<(unsigned)blocks, 256, 0, s>>>(in, n, out_dev);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_size_terms(const uint32_t* B, long long n, unsigned long long* rt,
