@@ -134,6 +134,9 @@ def dist_setup(n_gpus):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     pg = None
     if world > 1:
+        import torch
+        if torch.cuda.device_count() < world:  # every rank exits: no rank left waiting in a collective
+            raise SystemExit(f"bench.py: {world} ranks need {world} GPUs, {torch.cuda.device_count()} visible")
         import torch.distributed as dist
         dist.init_process_group("gloo")  # control plane only; data path is our NCCL comm
         pg = dist
