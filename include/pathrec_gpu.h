@@ -270,7 +270,7 @@ enum {
     PRC_EVAL_NORMALIZE = 1,     /* divide by the global record count (default on) */
     PRC_EVAL_WANT_GRAD = 2,
     PRC_EVAL_LEGACY_SCORE = 4,  /* pathstore.cpp:98-101 */
-    PRC_EVAL_SELF_NORMALIZE = 8,/* rejected: PRC_ERR_CONFIG (not on the recycling loop) */
+    PRC_EVAL_SELF_NORMALIZE = 8,/* divide by the mean correction factor (pathstore.cpp:334-359) */
     PRC_EVAL_PER_SPECIES = 16,  /* per-type gradients: grad_out holds n_species x V */
     PRC_EVAL_DETERMINISTIC = 32 /* bit-reproducible images (exact fixed-point pixel sums,
                                    two forward passes); prc_gpu_render always does this */

@@ -571,7 +571,7 @@ struct EvalOptions {
     bool normalize = true;
     bool want_grad = false;
     bool legacy_score = false;
-    bool self_normalize = false;  // rejected (std::invalid_argument)
+    bool self_normalize = false;  // divide by the mean correction factor (pathstore.cpp:334-359)
     const ImageSet* pixel_weights = nullptr;
     bool per_species = false;    // extension: per-type gradients (config (c))
     bool deterministic = false;  // extension: bit-reproducible images (render() always is)

@@ -234,6 +234,7 @@ struct prc_gpu_ctx {
     NvlsState* nvls = nullptr;
     DBuf<uint32_t> u32tmp;
     DBuf<int> err;
+    DBuf<double> selfn;  // self-normalisation sum (mean_correction)
     DBuf<unsigned> check;  // DScene::check (checked builds record range violations here)
     void* cub_tmp = nullptr;
     size_t cub_bytes = 0;
@@ -2247,13 +2248,13 @@ PRC_EXPORT void prc_gpu_store_free(prc_gpu_store* st) {
     delete st;
 }
 
+static double mean_correction(prc_gpu_ctx* c, prc_gpu_store* st, const EvalRun& er);
+
 PRC_EXPORT int prc_gpu_evaluate(prc_gpu_ctx* ctx, const prc_gpu_store* store,
                                 const prc_gpu_params* params, const prc_gpu_eval_opts* opts,
                                 prc_gpu_eval_result* res) {
     if (!ctx || !store || !res) return fail(PRC_ERR_INVALID, "prc_gpu_evaluate: null argument");
     const int flags = opts ? opts->flags : PRC_EVAL_NORMALIZE;
-    if (flags & PRC_EVAL_SELF_NORMALIZE)
-        return fail(PRC_ERR_CONFIG, "self_normalize is not supported by the recycling engine");
     if (store->ctx != ctx) return fail(PRC_ERR_INVALID, "prc_gpu_evaluate: the store belongs to another context");
     ABI_TRY
     auto _lk = begin(ctx);
@@ -2292,11 +2293,11 @@ PRC_EXPORT int prc_gpu_evaluate(prc_gpu_ctx* ctx, const prc_gpu_store* store,
     }
     copy_out(ctx, res->images, ctx->images.p, (size_t)ctx->n_pix);
     const DScene& s = ctx->dsc;
+    const int n_out = er.per_species ? s.n_species : 1;
+    const bool grad_beta_out = er.want_grad && s.has_medium && (s.unknown >= 0 || er.per_species) && ctx->grad_res;
     res->grad_kappa = res->grad_gamma = 0.0;
     if (er.want_grad) {
-        const int n_out = er.per_species ? s.n_species : 1;
-        if (s.has_medium && (s.unknown >= 0 || er.per_species) && ctx->grad_res)
-            copy_out(ctx, res->grad_beta, ctx->grad_res, (size_t)n_out * ctx->V);
+        if (grad_beta_out) copy_out(ctx, res->grad_beta, ctx->grad_res, (size_t)n_out * ctx->V);
         double gp[2] = {0, 0};
         CK(cudaMemcpyAsync(gp, ctx->g_phong.p, sizeof gp, cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaEventRecord(ctx->ev[5], ctx->stream));
@@ -2310,7 +2311,45 @@ PRC_EXPORT int prc_gpu_evaluate(prc_gpu_ctx* ctx, const prc_gpu_store* store,
     ctx->last_fwd_clamps = cl;
     res->clamp_events = cl;
     res->mean_correction = 1.0;
+    if (flags & PRC_EVAL_SELF_NORMALIZE) {
+        // pathstore.cpp:334-359: scale /= mean correction factor over the store; applied to
+        // the returned copies (the device images stay those of the cached forward)
+        const double mean = mean_correction(ctx, st, er);
+        res->mean_correction = mean;
+        if (mean > 0.0) {
+            const double inv = 1.0 / mean;
+            if (res->images)
+                for (long long i = 0; i < ctx->n_pix; ++i) res->images[i] *= inv;
+            if (grad_beta_out && res->grad_beta)
+                for (long long i = 0; i < (long long)n_out * ctx->V; ++i) res->grad_beta[i] *= inv;
+            res->grad_kappa *= inv;
+            res->grad_gamma *= inv;
+        }
+    }
     ABI_CATCH
+}
+
+// Mean correction_factor over the store (all ranks) under the context's current
+// evaluation fields (EvalOptions::self_normalize, pathstore.cpp:334-359).
+static double mean_correction(prc_gpu_ctx* c, prc_gpu_store* st, const EvalRun& er) {
+    cudaStream_t q = c->stream;
+    c->selfn.grow(1);
+    CK(cudaMemsetAsync(c->selfn.p, 0, sizeof(double), q));
+    CK(cudaMemsetAsync(c->err.p, 0, sizeof(int), q));
+    if (st->mat) {
+        CK(launch_mat_correction(c->dsc, st->mat_view(), st->m_ctx, c->selfn.p, c->err.p, q, &c->launches));
+    } else {
+        const EvalArgs ea = eval_args(c, st, er, c->phong.p);
+        CK(launch_correction(c->dsc, st->view(), ea, c->selfn.p, c->err.p, q, &c->launches));
+    }
+    c->allreduce(c->selfn.p, 1);
+    double sum = 0.0;
+    int errf = 0;
+    CK(cudaMemcpyAsync(&sum, c->selfn.p, sizeof sum, cudaMemcpyDeviceToHost, q));
+    CK(cudaMemcpyAsync(&errf, c->err.p, sizeof errf, cudaMemcpyDeviceToHost, q));
+    c->sync();
+    if (errf) throw Err(PRC_ERR_NUMERIC, "correction_factor: zero reference extinction at a vertex");
+    return st->n_global ? sum / (double)st->n_global : 1.0;
 }
 
 // ------------------------------------------------------------------ Algorithm 2 (device)

@@ -201,6 +201,53 @@ __global__ void __launch_bounds__(kMatTPB) k_mat_gradient(const __grid_constant_
     }
 }
 
+// correction_factor (pathstore.cpp:269-294) of every path over its stored spans, summed:
+// lr = -sum over all segments' spans (the escape segment included) of dbeta l, plus
+// log(ext_t) - log(ext_ref) at every volume vertex before the last; the path's factor is
+// exp(clamp(lr)), or 0 when ext_t vanishes.  *err: a vertex with zero reference
+// extinction (the reference throws).
+__global__ void __launch_bounds__(kMatTPB) k_mat_correction(const __grid_constant__ DScene sc,
+                                                            const __grid_constant__ MatView mv,
+                                                            const __grid_constant__ MatCtx m,
+                                                            double* __restrict__ sum, int* __restrict__ err) {
+    const unsigned long long p = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+    double c = 0.0;
+    if (p < mv.n) {
+        const unsigned long long r = mv.rec[p];
+        const unsigned long long v0 = mv.v_base[r], s0 = mv.s_base[r];
+        const int B = (int)(mv.v_base[r + 1] - v0) - 1;
+        double lr = 0.0;
+        bool zero = false;
+        for (int b = 1; b <= B; ++b) {
+            const unsigned long long vi = v0 + (unsigned long long)b;
+            if (sc.has_medium)
+                for (uint32_t k = mv.v_sb[vi]; k < mv.v_se[vi]; ++k)
+                    lr -= m.dbeta[mv.s_vox[s0 + k]] * mv.s_len[s0 + k];
+            if (b == B) break;
+            if (meta_kind(mv.v_meta[vi]) == VK_VOLUME) {
+                const int vox = mv.v_vox[vi];
+                const double ct = mv.v_ct[vi];
+                const double num = mat_ext_num_ref(sc, m, vox, ct);
+                double num_t = 0.0;
+                for (int j = 0; j < sc.n_species; ++j) num_t += m.t[j][vox] * phase_eval(sc.sp[j], ct);
+                if (num <= 0.0) {
+                    atomicExch(err, 1);
+                    zero = true;
+                    break;
+                }
+                if (num_t <= 0.0) {
+                    zero = true;
+                    break;
+                }
+                lr += log(num_t) - log(num);
+            }
+        }
+        c = zero ? 0.0 : exp(clampd(lr, -PRC_LOG_CLAMP, PRC_LOG_CLAMP));
+    }
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0 && c != 0.0) atomicAdd(sum, c);
+}
+
 __global__ void k_gather_u64(const uint32_t* __restrict__ perm, long long n,
                              const unsigned long long* __restrict__ src, unsigned long long* __restrict__ dst) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -233,6 +280,13 @@ cudaError_t launch_mat_gradient(const DScene& sc, const MatView& mv, const MatCt
                                 cudaStream_t s, unsigned long long* launches) {
     if (mv.n == 0) return cudaSuccess;
     k_mat_gradient<<<mat_grid((long long)mv.n), kMatTPB, 0, s>>>(sc, mv, m, ea);
+    MAT_LAUNCH_DONE();
+}
+
+cudaError_t launch_mat_correction(const DScene& sc, const MatView& mv, const MatCtx& m, double* sum, int* err,
+                                  cudaStream_t s, unsigned long long* launches) {
+    if (mv.n == 0) return cudaSuccess;
+    k_mat_correction<<<mat_grid((long long)mv.n), kMatTPB, 0, s>>>(sc, mv, m, sum, err);
     MAT_LAUNCH_DONE();
 }
 

@@ -1037,6 +1037,59 @@ __global__ void k_unpad_add(const __grid_constant__ DScene sc, const double* __r
     g_span[v] += acc;
 }
 
+// ------------------------------------------------------------------ self-normalisation
+// correction_factor (pathstore.cpp:269-294) of every path, summed (EvalOptions::
+// self_normalize, pathstore.cpp:334-359): lr = -sum over ALL segments (the escape segment
+// included) of the dbeta optical depth, plus log(ext_t) - log(ext_ref) at every volume
+// vertex before the last; exp(clamp(lr)), or 0 when ext_t vanishes.  The segments are
+// re-walked with the bit-exact DDA over the padded dbeta table (or the unpadded one).
+// *err: a vertex with zero reference extinction (the reference throws).
+__global__ void __launch_bounds__(kTPB) k_correction(const __grid_constant__ DScene sc,
+                                                     const __grid_constant__ StoreView st,
+                                                     const __grid_constant__ EvalArgs ea,
+                                                     double* __restrict__ sum, int* __restrict__ err) {
+    const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    double c = 0.0;
+    if (p < (long long)st.n) {
+        const int B = (int)st.B[p];
+        const unsigned long long rb = st.rec_base[p];
+        const unsigned rs = st.stride[p];
+        V3 xprev = mk(st.px[rb], st.py[rb], st.pz[rb]);
+        double lr = 0.0;
+        bool zero = false;
+        for (int b = 1; b <= B; ++b) {
+            const unsigned long long r = rb + (unsigned long long)b * rs;
+            if (sc.has_medium) {
+                const V3 d = mk(st.dx[r], st.dy[r], st.dz[r]);
+                lr -= sc.pad_walk ? dda_optical_depth_pad(sc, xprev, d, st.tt[r], ea.db_pad)
+                                  : dda_optical_depth(sc, xprev, d, st.tt[r], ea.dbeta);
+            }
+            if (b == B) break;
+            const uint32_t m = st.meta[r];
+            if (meta_kind(m) == VK_VOLUME) {
+                const int vox = st.vox[r];
+                const double ct = st.ct[r];
+                const double num = ext_num(sc, ea.sp_ref, vox, ct);
+                const double num_t = ext_num(sc, ea.sp_t, vox, ct);
+                if (num <= 0.0) {
+                    atomicExch(err, 1);
+                    zero = true;
+                    break;
+                }
+                if (num_t <= 0.0) {
+                    zero = true;
+                    break;
+                }
+                lr += log(num_t) - log(num);
+            }
+            xprev = mk(st.px[r], st.py[r], st.pz[r]);
+        }
+        c = zero ? 0.0 : exp(clampd(lr, -PRC_LOG_CLAMP, PRC_LOG_CLAMP));
+    }
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0 && c != 0.0) atomicAdd(sum, c);
+}
+
 // ------------------------------------------------------------------ event list (no medium)
 // Scenes without a medium have only surface interaction vertices and no LE walks; K4b over
 // the dense [det][i] cache is then bound by the latency of one cache load per (vertex,
@@ -1326,6 +1379,13 @@ cudaError_t launch_le_gradient(const DScene& sc, const VertexTable& vt, const Ev
         LAUNCH_DONE();
     }
     k_le_gradient<<<grid_for((long long)vt.n, kWF), kWF, 0, s>>>(sc, vt, ea, own, spread);
+    LAUNCH_DONE();
+}
+
+cudaError_t launch_correction(const DScene& sc, const StoreView& st, const EvalArgs& ea, double* sum, int* err,
+                              cudaStream_t s, unsigned long long* launches) {
+    if (st.n == 0) return cudaSuccess;
+    k_correction<<<grid_for((long long)st.n, kTPB), kTPB, 0, s>>>(sc, st, ea, sum, err);
     LAUNCH_DONE();
 }
 

@@ -271,12 +271,33 @@ def test_per_type_gradients(ctx, golden_dir, mode):
     assert grad_err(r.grad_beta[1], g["flip_pert_w_grad"]) <= GRAD_TOL
 
 
-def test_self_normalize_rejected(ctx, golden_dir):
-    scene = FIXTURES["tomo2"]["scene"]()
+@pytest.mark.parametrize("name", list(FIXTURES))
+@pytest.mark.parametrize("materialized", [False, True])
+def test_self_normalize_matches_reference(ctx, ref, golden_dir, name, materialized):
+    """EvalOptions::self_normalize (pathstore.cpp:334-359): images and gradients divided by
+    the mean correction_factor (pathstore.cpp:269-294, the escape segment's spans
+    included) over the store, and that mean reported; against the reference's
+    evaluate_store on its own store, recomputed and materialized imports."""
+    scene = FIXTURES[name]["scene"]()
     ctx.upload(scene)
-    st = ctx.load_store(str(golden_dir / "tomo2.pstr"))
-    with pytest.raises(PrcConfigError):
-        ctx.evaluate_store(scene, st, None, EvalOptions(self_normalize=True))
+    pstr = str(golden_dir / f"{name}.pstr")
+    st = ctx.load_store(pstr, materialized=materialized)
+    w = weight_patterns(scene)["w"]
+    p = perturbed(scene)
+    flags = abi.PRC_EVAL_NORMALIZE | abi.PRC_EVAL_SELF_NORMALIZE | abi.PRC_EVAL_WANT_GRAD
+    r = ref.evaluate(scene, pstr, p, flags, w)
+    for _ in range(2):  # the second call reuses the cached forward
+        g = ctx.evaluate_store(scene, st, p, EvalOptions(want_grad=True, pixel_weights=w, self_normalize=True))
+        assert scalar_err(g.mean_correction, r["mean_correction"]) <= 1e-6, (g.mean_correction, r["mean_correction"])
+        assert img_err(g.images, r["images"]) <= IMG_TOL
+        if scene.unknown_species() >= 0:
+            assert grad_err(g.grad_beta, r["grad"]) <= GRAD_TOL
+        else:
+            assert scalar_err(g.grad_kappa, r["grad_kappa"]) <= GRAD_TOL
+            assert scalar_err(g.grad_gamma, r["grad_gamma"]) <= GRAD_TOL
+    plain = ctx.evaluate_store(scene, st, p, EvalOptions())
+    assert plain.mean_correction == 1.0
+    assert np.allclose(plain.images / g.mean_correction, g.images, rtol=1e-12, atol=0.0)
 
 
 def test_pstr_errors(ctx, tmp_path):
