@@ -241,6 +241,12 @@ typedef struct {
 int prc_gpu_store_info_get(const prc_gpu_store* store, prc_gpu_store_info* out);
 /* Stream ids in storage order (PathStore::records[i].stream). */
 int prc_gpu_store_streams(const prc_gpu_store* store, uint64_t* out);
+/* correction_factor (pathstore.cpp:269-294) of every path of this shard under params_t
+ * (NULL: the scene's values) against the store's reference parameters, in storage order
+ * (prc_gpu_store_streams gives each position's stream id); out has prc_gpu_store_info.n
+ * entries.  The mean of these over the store is EvalOptions::self_normalize's divisor. */
+int prc_gpu_correction_factors(prc_gpu_ctx* ctx, const prc_gpu_store* store, const prc_gpu_params* params_t,
+                               double* out);
 /* Path sizes B in storage order. */
 int prc_gpu_store_sizes(const prc_gpu_store* store, uint32_t* out);
 /* PSTR v1 interchange (pathstore.cpp:410-516).  Export materialises every span and

@@ -2248,7 +2248,7 @@ PRC_EXPORT void prc_gpu_store_free(prc_gpu_store* st) {
     delete st;
 }
 
-static double mean_correction(prc_gpu_ctx* c, prc_gpu_store* st, const EvalRun& er);
+static double mean_correction(prc_gpu_ctx* c, prc_gpu_store* st, const EvalRun& er, double* per_path = nullptr);
 
 PRC_EXPORT int prc_gpu_evaluate(prc_gpu_ctx* ctx, const prc_gpu_store* store,
                                 const prc_gpu_params* params, const prc_gpu_eval_opts* opts,
@@ -2331,16 +2331,17 @@ PRC_EXPORT int prc_gpu_evaluate(prc_gpu_ctx* ctx, const prc_gpu_store* store,
 
 // Mean correction_factor over the store (all ranks) under the context's current
 // evaluation fields (EvalOptions::self_normalize, pathstore.cpp:334-359).
-static double mean_correction(prc_gpu_ctx* c, prc_gpu_store* st, const EvalRun& er) {
+static double mean_correction(prc_gpu_ctx* c, prc_gpu_store* st, const EvalRun& er, double* per_path) {
     cudaStream_t q = c->stream;
     c->selfn.grow(1);
     CK(cudaMemsetAsync(c->selfn.p, 0, sizeof(double), q));
     CK(cudaMemsetAsync(c->err.p, 0, sizeof(int), q));
     if (st->mat) {
-        CK(launch_mat_correction(c->dsc, st->mat_view(), st->m_ctx, c->selfn.p, c->err.p, q, &c->launches));
+        CK(launch_mat_correction(c->dsc, st->mat_view(), st->m_ctx, c->selfn.p, c->err.p, per_path, q,
+                                 &c->launches));
     } else {
         const EvalArgs ea = eval_args(c, st, er, c->phong.p);
-        CK(launch_correction(c->dsc, st->view(), ea, c->selfn.p, c->err.p, q, &c->launches));
+        CK(launch_correction(c->dsc, st->view(), ea, c->selfn.p, c->err.p, per_path, q, &c->launches));
     }
     c->allreduce(c->selfn.p, 1);
     double sum = 0.0;
@@ -2350,6 +2351,26 @@ static double mean_correction(prc_gpu_ctx* c, prc_gpu_store* st, const EvalRun& 
     c->sync();
     if (errf) throw Err(PRC_ERR_NUMERIC, "correction_factor: zero reference extinction at a vertex");
     return st->n_global ? sum / (double)st->n_global : 1.0;
+}
+
+PRC_EXPORT int prc_gpu_correction_factors(prc_gpu_ctx* ctx, const prc_gpu_store* store,
+                                          const prc_gpu_params* params_t, double* out) {
+    if (!ctx || !store || !out) return fail(PRC_ERR_INVALID, "prc_gpu_correction_factors: null argument");
+    if (store->ctx != ctx) return fail(PRC_ERR_INVALID, "prc_gpu_correction_factors: the store belongs to another context");
+    ABI_TRY
+    auto _lk = begin(ctx);
+    ctx->check_scene();
+    auto* st = const_cast<prc_gpu_store*>(store);
+    store_for_scene(ctx, st);
+    EvalRun er;
+    const Resolved r = resolve_params(ctx, params_t, st);
+    run_eval(ctx, st, r, er, nullptr);  // the evaluation fields under params_t
+    DBuf<double> pp;
+    pp.alloc(std::max<unsigned long long>(st->n, 1));
+    mean_correction(ctx, st, er, pp.p);
+    copy_out(ctx, out, pp.p, (size_t)st->n);
+    ctx->sync();
+    ABI_CATCH
 }
 
 // ------------------------------------------------------------------ Algorithm 2 (device)

@@ -257,9 +257,10 @@ cudaError_t launch_evc_forward(const DScene& sc, const EventList& el, const Eval
 cudaError_t launch_evc_gradient(const DScene& sc, const EventList& el, const EvalArgs& ea, double* own,
                                 cudaStream_t s, unsigned long long* launches);
 // Sum over the store of correction_factor (pathstore.cpp:269-294) under the current
-// context (EvalOptions::self_normalize); *err set on a zero reference extinction.
+// context (EvalOptions::self_normalize), and each path's factor into per_path[storage
+// position] when per_path is not NULL; *err set on a zero reference extinction.
 cudaError_t launch_correction(const DScene& sc, const StoreView& st, const EvalArgs& ea, double* sum, int* err,
-                              cudaStream_t s, unsigned long long* launches);
+                              double* per_path, cudaStream_t s, unsigned long long* launches);
 // K5a: per-path suffix pass (segment spans, continuation scores) from own[iv].
 cudaError_t launch_path_gradient(const DScene& sc, const StoreView& st, const EvalArgs& ea,
                                  const double* own, cudaStream_t s, unsigned long long* launches);
@@ -332,7 +333,7 @@ cudaError_t launch_mat_gradient(const DScene& sc, const MatView& mv, const MatCt
                                 cudaStream_t s, unsigned long long* launches);
 // correction_factor over the stored spans, summed into *sum (self_normalize)
 cudaError_t launch_mat_correction(const DScene& sc, const MatView& mv, const MatCtx& m, double* sum, int* err,
-                                  cudaStream_t s, unsigned long long* launches);
+                                  double* per_path, cudaStream_t s, unsigned long long* launches);
 // dst[i] = src[perm[i]]
 cudaError_t launch_gather_u64(const uint32_t* perm, long long n, const unsigned long long* src,
                               unsigned long long* dst, cudaStream_t s, unsigned long long* launches);

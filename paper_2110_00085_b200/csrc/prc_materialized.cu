@@ -209,7 +209,8 @@ __global__ void __launch_bounds__(kMatTPB) k_mat_gradient(const __grid_constant_
 __global__ void __launch_bounds__(kMatTPB) k_mat_correction(const __grid_constant__ DScene sc,
                                                             const __grid_constant__ MatView mv,
                                                             const __grid_constant__ MatCtx m,
-                                                            double* __restrict__ sum, int* __restrict__ err) {
+                                                            double* __restrict__ sum, int* __restrict__ err,
+                                                            double* __restrict__ per_path) {
     const unsigned long long p = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
     double c = 0.0;
     if (p < mv.n) {
@@ -243,6 +244,7 @@ __global__ void __launch_bounds__(kMatTPB) k_mat_correction(const __grid_constan
             }
         }
         c = zero ? 0.0 : exp(clampd(lr, -PRC_LOG_CLAMP, PRC_LOG_CLAMP));
+        if (per_path) per_path[p] = c;
     }
     for (int o = 16; o > 0; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
     if ((threadIdx.x & 31) == 0 && c != 0.0) atomicAdd(sum, c);
@@ -284,9 +286,9 @@ cudaError_t launch_mat_gradient(const DScene& sc, const MatView& mv, const MatCt
 }
 
 cudaError_t launch_mat_correction(const DScene& sc, const MatView& mv, const MatCtx& m, double* sum, int* err,
-                                  cudaStream_t s, unsigned long long* launches) {
+                                  double* per_path, cudaStream_t s, unsigned long long* launches) {
     if (mv.n == 0) return cudaSuccess;
-    k_mat_correction<<<mat_grid((long long)mv.n), kMatTPB, 0, s>>>(sc, mv, m, sum, err);
+    k_mat_correction<<<mat_grid((long long)mv.n), kMatTPB, 0, s>>>(sc, mv, m, sum, err, per_path);
     MAT_LAUNCH_DONE();
 }
 

@@ -1047,7 +1047,8 @@ __global__ void k_unpad_add(const __grid_constant__ DScene sc, const double* __r
 __global__ void __launch_bounds__(kTPB) k_correction(const __grid_constant__ DScene sc,
                                                      const __grid_constant__ StoreView st,
                                                      const __grid_constant__ EvalArgs ea,
-                                                     double* __restrict__ sum, int* __restrict__ err) {
+                                                     double* __restrict__ sum, int* __restrict__ err,
+                                                     double* __restrict__ per_path) {
     const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     double c = 0.0;
     if (p < (long long)st.n) {
@@ -1085,6 +1086,7 @@ __global__ void __launch_bounds__(kTPB) k_correction(const __grid_constant__ DSc
             xprev = mk(st.px[r], st.py[r], st.pz[r]);
         }
         c = zero ? 0.0 : exp(clampd(lr, -PRC_LOG_CLAMP, PRC_LOG_CLAMP));
+        if (per_path) per_path[p] = c;
     }
     for (int o = 16; o > 0; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
     if ((threadIdx.x & 31) == 0 && c != 0.0) atomicAdd(sum, c);
@@ -1383,9 +1385,9 @@ cudaError_t launch_le_gradient(const DScene& sc, const VertexTable& vt, const Ev
 }
 
 cudaError_t launch_correction(const DScene& sc, const StoreView& st, const EvalArgs& ea, double* sum, int* err,
-                              cudaStream_t s, unsigned long long* launches) {
+                              double* per_path, cudaStream_t s, unsigned long long* launches) {
     if (st.n == 0) return cudaSuccess;
-    k_correction<<<grid_for((long long)st.n, kTPB), kTPB, 0, s>>>(sc, st, ea, sum, err);
+    k_correction<<<grid_for((long long)st.n, kTPB), kTPB, 0, s>>>(sc, st, ea, sum, err, per_path);
     LAUNCH_DONE();
 }
 

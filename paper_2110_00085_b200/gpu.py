@@ -96,6 +96,7 @@ def load_library(path: Optional[str] = None):
         "prc_gpu_sort_by_size": [vp, vp],
         "prc_gpu_store_info_get": [vp, C.POINTER(abi.StoreInfo)],
         "prc_gpu_store_streams": [vp, _u64p],
+        "prc_gpu_correction_factors": [vp, vp, vp, _dp],
         "prc_gpu_store_sizes": [vp, _u32p],
         "prc_gpu_store_export_pstr": [vp, vp, C.c_char_p],
         "prc_gpu_store_import_pstr": [vp, C.c_char_p, C.POINTER(vp)],
@@ -368,6 +369,16 @@ class Context:
             if opt.per_species:
                 g = g.reshape(n_out, s.voxel_count)
         return EvalResult(img, g, r.grad_kappa, r.grad_gamma, int(r.clamp_events), r.mean_correction)
+
+    def correction_factors(self, scene: Optional[Scene], store: PathStore,
+                           params: Optional[ParamSet] = None) -> np.ndarray:
+        """correction_factor (pathstore.cpp:269-294) of every path of the store, in storage
+        order (store.streams() gives the stream ids)."""
+        self._use(scene)
+        ph = ParamsHolder(params)
+        out = np.zeros(max(1, len(store)))
+        _check(_lib.prc_gpu_correction_factors(self.ptr, store.ptr, ph.ptr, _ptr(out, _dp)))
+        return out[:len(store)]
 
     def recycled_render(self, scene: Optional[Scene], store: PathStore,
                         params: Optional[ParamSet] = None) -> np.ndarray:

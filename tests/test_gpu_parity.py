@@ -933,3 +933,48 @@ def test_ragged_store_sizes(ctx, name):
             r = ctx.evaluate_store(scene, st, None, EvalOptions(deterministic=True))
             assert np.array_equal(r.images, rr.images), (name, n)
         st.free()
+
+
+def test_correction_factors_known_answers(ctx, tmp_path):
+    """correction_factor (pathstore.cpp:269-294) on the device, the reference's own test
+    cases (test_pathstore.cpp:29-85) on a homogeneous HG cube: exactly 1 at the sampling
+    parameters; c^B exp(-(c-1) beta L) under uniform scaling by c (B volume scatters, L the
+    path's length through the grid, from the exported spans; the device keeps the
+    per-voxel fields in fp32, so 1e-6 instead of the reference's 1e-9); exactly 1 when
+    only a voxel the path never crosses changes; 0 when a scatter vertex's extinction
+    vanishes."""
+    from tests.pstr import read as read_pstr
+    s = S.homogeneous_cube(3.0, 0.9, "hg", 0.5, grid_n=4)
+    s.species[0].unknown = True
+    ctx.upload(s)
+    st = ctx.render(s, RenderOptions(n_paths=400, seed=7, keep_paths=True, max_bounces=200)).store
+    pstr = str(tmp_path / "c.pstr")
+    st.save(pstr)
+    recs = {int(r["stream"]): r for r in read_pstr(pstr)["records"]}
+    order = [recs[int(k)] for k in st.streams()]
+    uref = np.full(64, 3.0)
+    f1 = ctx.correction_factors(s, st, S.ParamSet(uref))
+    assert np.all(f1 == 1.0)
+    c = 1.3
+    fc = ctx.correction_factors(s, st, S.ParamSet(uref * c))
+    for f, rec in zip(fc, order):
+        n_scat = int(np.sum(rec["vertices"]["kind"] == 1))
+        L = float(rec["spans"]["length"].sum())
+        expected = c ** n_scat * np.exp(-(c - 1.0) * 3.0 * L)
+        assert abs(f - expected) <= 1e-6 * expected, (f, expected)
+    checked = killed = 0
+    for i, rec in enumerate(order[:60]):
+        touched = set(int(v) for v in rec["spans"]["voxel"]) | set(int(v) for v in rec["le_spans"]["voxel"])
+        free = [v for v in range(64) if v not in touched]
+        if free:
+            t = uref.copy()
+            t[free[0]] *= 5.0
+            assert ctx.correction_factors(s, st, S.ParamSet(t))[i] == 1.0
+            checked += 1
+        scat = [int(v["voxel"]) for v in rec["vertices"] if v["kind"] == 1]
+        if scat and killed < 5:
+            t = uref.copy()
+            t[scat[-1]] = 0.0
+            assert ctx.correction_factors(s, st, S.ParamSet(t))[i] == 0.0
+            killed += 1
+    assert checked > 0 and killed > 0
