@@ -1145,16 +1145,19 @@ void run_forward(prc_gpu_ctx* c, prc_gpu_store* st, const Resolved& r, const Eva
     CK(cudaEventRecord(c->ev[3], q));
 }
 
-// K5b lane spreading by interaction vertices per voxel d.  Round 2, K5b ms at spread
-// 4 / 16 / 32 / 64: (b) 1e8 paths at 128^3 (d = 150) 672 / 603 / 602 / 607, (c) (d = 151)
-// - / 714 / 704 / 705; 3e7 paths (d = 45) 188 / 185 / 189 / -; 1e7 paths (d = 15)
-// 64.5 / 67.3 / - / 74.0; (e) 256^3 (d = 23) 1499 / 1524 / 1584 / 1658; (a) 32^3 (d = 96,
-// 32 copies) 2.28 / 2.39 / 2.47 / 2.52.  Dense tables want lanes far apart (same-voxel
-// reductions), sparse ones want them close (coherent walks).
+// K5b lane spreading.  Lanes far apart in Morton order avoid same-voxel reductions in one
+// RED instruction; lanes close together walk coherent rays.  The contention scale is the
+// interaction vertices per voxel d per gradient copy C.  Round 2, K5b ms at spread
+// 4 / 16 / 32 / 64: (b) 1e8 paths at 128^3 (d = 150, C = 8) 672 / 603 / 602 / 607, (c)
+// (d = 151) - / 714 / 704 / 705; 5e7 paths (d = 75) 322 / 302 / 307 / -; 3e7 paths (d = 45)
+// 188 / 185 / 189 / -; 2.5e7 (d = 37) 157 / 155 / - / -; 1e7 paths (d = 15) 64.5 / 67.3 /
+// - / 74.0; (e) 256^3 (d = 23, C = 8) 1499 / 1524 / 1584 / 1658; (a) 32^3 (d = 96, C = 32)
+// 2.28 / 2.39 / 2.47 / 2.52.
 int auto_spread(const prc_gpu_ctx* c, const prc_gpu_store* st) {
     if (c->spread > 0) return c->spread;
     const double d = (double)st->n_iv / (double)std::max<long long>(c->V, 1);
-    return d >= 120.0 ? 32 : 4;
+    const double q = d / (double)std::max(1, c->g_pad_copies);
+    return q >= 15.0 ? 32 : q >= 4.0 ? 16 : 4;
 }
 
 // K5 gradient with weights ea.weights, then its reduction over ranks and the combination
