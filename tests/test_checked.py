@@ -60,6 +60,16 @@ for mapping in ({"mode": 0, "packet": 3}, {"mode": 0, "packet": 1}, {"mode": 0, 
                 n += 1
             st.free()
     ctx.set_option("mode", 0); ctx.set_option("packet", 3); ctx.set_option("pad", 1)
+# self-normalisation and the per-path correction factors (all segments re-walked)
+for name in FIXTURES:
+    sc = FIXTURES[name]["scene"]()
+    ctx.upload(sc)
+    for mat in (False, True):
+        st = ctx.load_store(os.path.join(tmp, name + ".pstr"), materialized=mat)
+        ctx.evaluate_store(sc, st, perturbed(sc), EvalOptions(want_grad=True, self_normalize=True))
+        ctx.correction_factors(sc, st, perturbed(sc))
+        clean((name, "self_normalize", mat))
+        st.free()
 # per-type gradients, deterministic images, the driver loop
 sc = FIXTURES["tomo2"]["scene"]()
 ctx.upload(sc)
