@@ -177,20 +177,22 @@ int prc_gpu_ctx_rank(const prc_gpu_ctx* ctx, int* rank, int* world);
  * that shares the GPU with another allocator (e.g. torch) can call it after freeing
  * stores. */
 int prc_gpu_release_cached_memory(void);
-/* Engine knobs: "mode" 0 = event-major wavefront over Morton-ordered interaction
- * vertices (default), 1 = fused thread-per-path (the paper's mapping); "packet" 1..4 =
- * LE rays per thread walked in lockstep by the gradient kernel (default 3); "spread" =
- * Morton distance between the packets of one warp (default 0: by vertex density); "per_species" 1 = the
- * device-resident iteration (prc_gpu_opt_step) computes per-type gradients of every
- * species (config (c)); the optimiser still updates the unknown species; "pad" 0 turns
- * off the guard-free walks over the padded voxel layout (default 1; same results);
- * "grad_copies" = copies of the padded gradient the gradient kernel reduces into (0 =
- * default: 8, fewer when they would exceed 2 GB; applied at the next scene upload; same
- * results up to the order of floating-point sums); "events" 0 turns off the compact
- * event list of scenes without a medium (default 1: after the first forward over a store,
- * forwards and gradients run over its events only; same event values); "nvls" 1 =
- * images and gradients reduced over ranks by NVLS multicast (2 = the fold without
- * multicast, one rank; applied at the next scene upload). */
+/* Engine knobs (all give the same results up to the order of floating-point sums):
+ * - "mode": 0 = event-major wavefront over Morton-ordered interaction vertices
+ *   (default), 1 = fused thread-per-path (the paper's mapping);
+ * - "packet" 1..4: LE rays per thread walked in lockstep by the gradient kernel (default 3);
+ * - "spread": Morton distance between the packets of one warp (default 0: chosen from
+ *   the vertex density per gradient copy);
+ * - "per_species" 1: the device-resident iteration (prc_gpu_opt_step) computes per-type
+ *   gradients of every species (config (c)); the optimiser still updates the unknown one;
+ * - "pad" 0: no guard-free walks over the padded voxel layout (default 1);
+ * - "grad_copies": copies of the padded gradient the gradient kernel reduces into (0 =
+ *   default: 8, up to 32 while they fit in 64 MB, fewer when they would exceed 2 GB;
+ *   applied at the next scene upload);
+ * - "events" 0: no compact event list for scenes without a medium (default 1: after the
+ *   first forward over a store, forwards and gradients run over its events only);
+ * - "nvls" 1: images and gradients reduced over ranks by NVLS multicast (2 = the fold
+ *   without multicast, one rank; applied at the next scene upload). */
 int prc_gpu_ctx_set_option(prc_gpu_ctx* ctx, const char* key, int64_t value);
 
 /* Uploads (and validates, finalizes) the scene; replaces any previous scene and
