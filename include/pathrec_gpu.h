@@ -160,7 +160,9 @@ int prc_gpu_nccl_unique_id(void* out128);
 /* nccl_id NULL with world > 1: a detached shard without a communicator.  The context
  * traces / imports rank `rank`'s stream range and every result it returns (images,
  * gradients, clamp and truncation counts) is that shard's partial sum, still normalised by
- * the global path count; the caller reduces them (e.g. over MPI or torch.distributed). */
+ * the global path count; the caller reduces them (e.g. over MPI or torch.distributed).
+ * With PRC_EVAL_SELF_NORMALIZE a detached shard returns its results undivided and its
+ * partial mean_correction (shard sum / global count): the caller sums both and divides. */
 int prc_gpu_ctx_create_rank(int device, int rank, int world, const void* nccl_id,
                             prc_gpu_ctx** out);
 /* The contiguous stream range [lo, hi) rank `rank` of `world` owns out of n paths

@@ -2319,7 +2319,10 @@ PRC_EXPORT int prc_gpu_evaluate(prc_gpu_ctx* ctx, const prc_gpu_store* store,
         // the returned copies (the device images stay those of the cached forward)
         const double mean = mean_correction(ctx, st, er);
         res->mean_correction = mean;
-        if (mean > 0.0) {
+        // a detached shard (world > 1, no communicator) holds a partial sum only: it returns
+        // its partial mean (shard sum / global count) and leaves the division to the caller
+        const bool detached = ctx->world > 1 && !ctx->comm;
+        if (mean > 0.0 && !detached) {
             const double inv = 1.0 / mean;
             if (res->images)
                 for (long long i = 0; i < ctx->n_pix; ++i) res->images[i] *= inv;

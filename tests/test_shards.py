@@ -65,6 +65,32 @@ def test_detached_shards_sum_to_the_single_context_result(ctx, golden_dir, world
     assert rel(img, golden("tomo2")["pert_w_images"]) <= 1e-5
 
 
+def test_detached_shards_self_normalize(ctx, golden_dir):
+    """Self-normalisation over detached shards: each returns its undivided partial sums
+    and its partial mean correction factor; their sums give the single-context result."""
+    scene = FIXTURES["tomo2"]["scene"]()
+    p = perturbed(scene)
+    opt = EvalOptions(self_normalize=True)
+    ctx.upload(scene)
+    full = ctx.load_store(str(golden_dir / "tomo2.pstr"))
+    ref = ctx.evaluate_store(scene, full, p, opt)
+    img = np.zeros_like(ref.images)
+    mean = 0.0
+    for r in range(3):
+        c = Context(0, r, 3)
+        try:
+            c.upload(scene)
+            st = c.load_store(str(golden_dir / "tomo2.pstr"))
+            part = c.evaluate_store(scene, st, p, opt)
+            img += part.images
+            mean += part.mean_correction
+            st.free()
+        finally:
+            c.close()
+    assert abs(mean - ref.mean_correction) <= 1e-12 * ref.mean_correction
+    assert rel(img / mean, ref.images) <= 1e-12
+
+
 def test_detached_shard_traces_are_the_single_trace(ctx):
     scene = S.cloud_scene(16, 12, 12)
     n = 50_001
