@@ -33,9 +33,6 @@ constexpr int kWF = 256;  // vertices per CTA in the wavefront kernels
 #ifndef PRC_FWD_TPB
 #define PRC_FWD_TPB 128
 #endif
-#ifndef PRC_K4B_FAST  // A/B: the specialised K4b (k_le_forward_fast) on / off
-#define PRC_K4B_FAST 0  // measured: generic K4b 373 vs 377 ms at (b), fast 1.43 vs 1.48 ms at (a)
-#endif
 constexpr int kFwdTPB = PRC_FWD_TPB;  // K4b: vertices per CTA (128 x 8 CTAs 379.6 ms vs 256 x 4 382.3)
 #ifndef PRC_PATH_TPB
 #define PRC_PATH_TPB 128
@@ -391,65 +388,6 @@ __global__ void __launch_bounds__(kFwdTPB, kFwdMinBlocks) k_le_forward(const __g
     if ((threadIdx.x & 31) == 0 && clamps) atomicAdd(ea.clamps, (unsigned long long)clamps);
 }
 
-// K4b for the common scene class once the event cache is built: one species with the
-// fixed-point event term, no surfaces, padded walks, geo_ready.  Every interaction vertex
-// is a volume scatter and every event's pixel and c1 come from the cache, so an event is
-// its connection ray, the walk and the exp -- the general kernel's pixel_of, surface,
-// phase and multi-species code is not compiled in (the same expression, the same bits).
-__global__ void __launch_bounds__(kFwdTPB, kFwdMinBlocks) k_le_forward_fast(const __grid_constant__ DScene sc,
-                                                                          const __grid_constant__ VertexTable vt,
-                                                                          const __grid_constant__ EvalArgs ea,
-                                                                          const double* __restrict__ lp) {
-    const unsigned long long i = (unsigned long long)blockIdx.x * kFwdTPB + threadIdx.x;
-    const bool act = i < vt.n;
-    double lvol = -INFINITY;  // lp - log(beta_ref) + log(beta_t), as k_le_forward's lbase / lvol
-    if (act) {
-        const int vox = vt.vox[i];
-        const double lpv = lp[vt.iv[i]];
-        PRC_CHECK(sc, lpv == -INFINITY || (vox >= 0 && vox < sc.V), CHK_VOXEL);
-        if (lpv != -INFINITY) {
-            const double den = (double)ea.br_tot[vox];
-            if (den > 0.0) {
-                const double lbase = lpv - log(den);
-                const double bt = (double)ea.sp_t[vox];
-                if (bt > 0.0) lvol = lbase + log(bt);
-            }
-        }
-    }
-    unsigned clamps = 0;
-    for (int k = 0; k < sc.n_det; ++k) {
-        const unsigned long long e = (unsigned long long)k * vt.n + i;
-        float val = 0.0f;
-#ifdef PRC_K4B_XTOP
-        const V3 x = act ? mk(vt.x[i], vt.y[i], vt.z[i]) : mk(0.0, 0.0, 0.0);
-#endif
-        if (lvol != -INFINITY) {
-            const int pix = vt.ev_pix[e];
-            const int32_t q = vt.ev_c1[e];
-            if (pix >= 0 && q != INT32_MIN) {
-                double logval = lvol + c1_dequant(sc, q);
-#ifndef PRC_K4B_XTOP
-                const V3 x = mk(vt.x[i], vt.y[i], vt.z[i]);
-#endif
-                const V3 to_det = ld3(sc.det[k].pos) - x;
-                const double r = norm3(to_det);
-                const double inv_r = 1.0 / r;
-                logval -= dda_optical_depth_pad(sc, x, to_det * inv_r, r, ea.bt_pad);
-                if (logval > PRC_LOG_CLAMP || logval < -PRC_LOG_CLAMP) {
-                    logval = clampd(logval, -PRC_LOG_CLAMP, PRC_LOG_CLAMP);
-                    ++clamps;
-                }
-                const double contrib = exp(logval) * (inv_r * inv_r) * sc.prefactor;
-                val = (float)contrib;
-                if (contrib != 0.0) image_add(sc, ea, sc.det[k].img_off + pix, contrib);
-            }
-        }
-        if (act) vt.ev_val[e] = val;
-    }
-    for (int o = 16; o > 0; o >>= 1) clamps += __shfl_down_sync(0xffffffffu, clamps, o);
-    if ((threadIdx.x & 31) == 0 && clamps) atomicAdd(ea.clamps, (unsigned long long)clamps);
-}
-
 // ------------------------------------------------------------------ K5b LE gradient
 __device__ __forceinline__ double score_j(const DScene& sc, const EvalArgs& ea, int j, int vox,
                                           double c, double num) {
@@ -598,11 +536,6 @@ struct PRay {
         return e;
     }
 };
-
-// fp64 reduction x into *a, unconditional.
-__device__ __forceinline__ void red_add_u(double* a, double x) {
-    asm volatile("red.global.add.f64 [%0], %1;" ::"l"(a), "d"(x) : "memory");
-}
 
 // fp64 reduction x into *a when e, as one predicated RED.
 __device__ __forceinline__ void red_add_p(bool e, double* a, double x) {
@@ -764,10 +697,6 @@ __global__ void __launch_bounds__(kGradTPB, M == 2 ? PRC_GRAD2_MINB : (M == 3 ? 
                 RED_ADD_IF(sc, g, ea.g_pad_stride, same ? -1 : v1, x1);
             }
         } else if (M == 3) {  // hand-scheduled triple (the default packet)
-#ifdef PRC_K5B_UNCOND
-            // a voxel of the padded table's iz = 0 border plane, spread over threads
-            const long long dummy_off = ((long long)blockIdx.x * blockDim.x + threadIdx.x) % sc.pnxny;
-#endif
             PRay R0, R1, R2;
             if (S[0].alive) R0.from(S[0], g, cf[0]); else R0.dead(g);
             if (S[1].alive) R1.from(S[1], g, cf[1]); else R1.dead(g);
@@ -796,19 +725,9 @@ __global__ void __launch_bounds__(kGradTPB, M == 2 ? PRC_GRAD2_MINB : (M == 3 ? 
                 const bool s10 = e0 && e1 && l1 == l0;
                 const bool s20 = e0 && e2 && l2 == l0;
                 const bool s21 = e1 && e2 && l2 == l1 && !s20;
-#ifdef PRC_K5B_UNCOND  // A/B: every slot reduces, disabled ones add 0 into a border voxel
-                {
-                    double* const dmy = g + dummy_off;
-                    const bool f1 = e1 && !s10, f2 = e2 && !s20 && !s21;
-                    red_add_u(e0 ? a0 : dmy, e0 ? x0 + (s10 ? x1 : 0.0) + (s20 ? x2 : 0.0) : 0.0);
-                    red_add_u(f1 ? a1 : dmy, f1 ? x1 + (s21 ? x2 : 0.0) : 0.0);
-                    red_add_u(f2 ? a2 : dmy, f2 ? x2 : 0.0);
-                }
-#else
                 red_add_p(e0, a0, x0 + (s10 ? x1 : 0.0) + (s20 ? x2 : 0.0));
                 red_add_p(e1 && !s10, a1, x1 + (s21 ? x2 : 0.0));
                 red_add_p(e2 && !s20 && !s21, a2, x2);
-#endif
             };
             while (R0.alive || R1.alive || R2.alive) pstep3();  // (two steps per trip: same time)
         } else if (M == 4) {  // hand-scheduled quad
@@ -1348,8 +1267,6 @@ cudaError_t launch_le_forward(const DScene& sc, const VertexTable& vt, const Eva
     if (vt.n == 0) return cudaSuccess;
     if (sc.scache)
         k_le_forward<true><<<grid_for((long long)vt.n, kFwdTPB), kFwdTPB, 0, s>>>(sc, vt, ea, lp);
-    else if (PRC_K4B_FAST && vt.geo_ready && sc.c1_fast && sc.n_surf == 0 && sc.pad_walk && sc.has_medium)
-        k_le_forward_fast<<<grid_for((long long)vt.n, kFwdTPB), kFwdTPB, 0, s>>>(sc, vt, ea, lp);
     else
         k_le_forward<false><<<grid_for((long long)vt.n, kFwdTPB), kFwdTPB, 0, s>>>(sc, vt, ea, lp);
     LAUNCH_DONE();
