@@ -2346,6 +2346,9 @@ static double mean_correction(prc_gpu_ctx* c, prc_gpu_store* st, const EvalRun& 
         CK(launch_mat_correction(c->dsc, st->mat_view(), st->m_ctx, c->selfn.p, c->err.p, per_path, q,
                                  &c->launches));
     } else {
+        // the padded dbeta table is refreshed by mode-0 forwards only (run_forward)
+        if (c->mode != 0 && c->dsc.pad_walk)
+            CK(launch_pad_tables(c->dsc, c->bt_tot.p, c->dbeta.p, c->bt_pad.p, c->db_pad.p, q, &c->launches));
         const EvalArgs ea = eval_args(c, st, er, c->phong.p);
         CK(launch_correction(c->dsc, st->view(), ea, c->selfn.p, c->err.p, per_path, q, &c->launches));
     }

@@ -273,12 +273,14 @@ def test_per_type_gradients(ctx, golden_dir, mode):
 
 @pytest.mark.parametrize("name", list(FIXTURES))
 @pytest.mark.parametrize("materialized", [False, True])
-def test_self_normalize_matches_reference(ctx, ref, golden_dir, name, materialized):
+@pytest.mark.parametrize("path_mode", [0, 1])
+def test_self_normalize_matches_reference(ctx, ref, golden_dir, name, materialized, path_mode):
     """EvalOptions::self_normalize (pathstore.cpp:334-359): images and gradients divided by
     the mean correction_factor (pathstore.cpp:269-294, the escape segment's spans
     included) over the store, and that mean reported; against the reference's
     evaluate_store on its own store, recomputed and materialized imports."""
     scene = FIXTURES[name]["scene"]()
+    ctx.set_option("mode", path_mode)
     ctx.upload(scene)
     pstr = str(golden_dir / f"{name}.pstr")
     st = ctx.load_store(pstr, materialized=materialized)
@@ -296,6 +298,7 @@ def test_self_normalize_matches_reference(ctx, ref, golden_dir, name, materializ
             assert scalar_err(g.grad_kappa, r["grad_kappa"]) <= GRAD_TOL
             assert scalar_err(g.grad_gamma, r["grad_gamma"]) <= GRAD_TOL
     plain = ctx.evaluate_store(scene, st, p, EvalOptions())
+    ctx.set_option("mode", 0)
     assert plain.mean_correction == 1.0
     assert np.allclose(plain.images / g.mean_correction, g.images, rtol=1e-12, atol=0.0)
 
