@@ -142,6 +142,20 @@ void cache_free(void* p, size_t cap) {
     c.blocks.push_back({p, cap, dev});
 }
 
+}  // namespace
+
+cudaError_t prc_malloc_retry(void** p, size_t bytes) {
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e != cudaErrorMemoryAllocation) return e;
+    cudaGetLastError();
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cache_release(dev);
+    return cudaMalloc(p, bytes);
+}
+
+namespace {
+
 template <class T>
 struct DBuf {  // owning device buffer (BlockCache)
     T* p = nullptr;

@@ -1011,7 +1011,7 @@ cudaError_t scan_u64(const unsigned long long* in, unsigned long long* out, long
     need = need > 0 ? need : sizeof(unsigned long long);
     if (need > *tmp_bytes) {
         if (*tmp) cudaFree(*tmp);
-        cudaError_t e = cudaMalloc(tmp, need);
+        cudaError_t e = prc_malloc_retry(tmp, need);
         if (e != cudaSuccess) {
             *tmp = nullptr;
             *tmp_bytes = 0;

@@ -115,6 +115,10 @@ struct TraceArgs {
     RecordsOut rec;
 };
 
+// cudaMalloc that, when the device is out of memory, first hands the engine's cached
+// blocks (prc_capi.cu, BlockCache) back to the driver and retries.
+cudaError_t prc_malloc_retry(void** p, size_t bytes);
+
 // ---- launchers (return cudaError_t); `launches` counts kernels issued -------------
 // Padded layout: bt_pad/db_pad interiors <- bt_tot/dbeta (borders stay zero), and
 // g_span += interior of g_pad (all copies).

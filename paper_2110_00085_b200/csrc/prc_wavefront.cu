@@ -1235,7 +1235,7 @@ cudaError_t sort_pairs_u32(const uint32_t* ki, uint32_t* ko, const uint32_t* vi,
     if (e != cudaSuccess) return e;
     if (need > *tmp_bytes) {
         if (*tmp) cudaFree(*tmp);
-        e = cudaMalloc(tmp, need);
+        e = prc_malloc_retry(tmp, need);
         if (e != cudaSuccess) {
             *tmp = nullptr;
             *tmp_bytes = 0;
