@@ -981,3 +981,16 @@ def test_correction_factors_known_answers(ctx, tmp_path):
             assert ctx.correction_factors(s, st, S.ParamSet(t))[i] == 0.0
             killed += 1
     assert checked > 0 and killed > 0
+
+
+def test_engine_options_validated(ctx):
+    """Context knobs (include/pathrec_gpu.h): out-of-range values and unknown keys are
+    PRC_ERR_CONFIG, valid ones are accepted (and restored)."""
+    for key, bad in (("mode", 2), ("packet", 0), ("packet", 5), ("spread", -1), ("spread", 5000),
+                     ("grad_copies", 65), ("nvls", 3), ("no_such_option", 1)):
+        with pytest.raises(PrcConfigError):
+            ctx.set_option(key, bad)
+    for key, good, default in (("spread", 0, 0), ("spread", 16, 0), ("events", 0, 1), ("grad_copies", 4, 0),
+                               ("packet", 2, 3), ("pad", 0, 1)):
+        ctx.set_option(key, good)
+        ctx.set_option(key, default)
