@@ -1,4 +1,4 @@
-"""Parity at the BASELINE.json configurations' geometry (SURVEY §8(d) (a), (b), (c)).
+"""Parity at the BASELINE.json configurations' geometry (SURVEY §8(d) (a)-(e)).
 
 The fixture tests (test_gpu_parity.py) use 5^3-12^3 grids.  Here the device path runs on
 the benchmarked scenes themselves: 32^3 / 9 x 64^2 (a), 128^3 / 9 x 128^2 (b) and the
@@ -49,6 +49,7 @@ CONFIGS = {
     "a": dict(scene=lambda: S.cloud_scene(32, 64, 64), n=20_000),
     "b": dict(scene=lambda: S.cloud_scene(128, 128, 128), n=8_000),
     "c": dict(scene=lambda: S.cloud_scene(128, 128, 128, two_species=True), n=6_000),
+    "e": dict(scene=lambda: S.cloud_scene(256, 128, 128), n=4_000),
 }
 
 
@@ -62,7 +63,7 @@ def _patch_ref_beta(path, beta):
         f.write(np.ascontiguousarray(beta, dtype="<f8").tobytes())
 
 
-@pytest.mark.parametrize("cfg", ["a", "b", "c"])
+@pytest.mark.parametrize("cfg", ["a", "b", "c", "e"])
 def test_config_store_matches_reference(ctx, ref, tmp_path, cfg):
     scene = CONFIGS[cfg]["scene"]()
     n = CONFIGS[cfg]["n"]
