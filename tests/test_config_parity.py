@@ -128,6 +128,31 @@ def test_reference_written_config_a_store(ctx, ref, tmp_path):
     assert e_img <= IMG_TOL and e_grad <= GRAD_TOL
 
 
+@pytest.mark.parametrize("materialized", [False, True])
+def test_reference_written_config_d_store(ctx, ref, tmp_path, materialized):
+    """A reflectometry store traced and sorted by the reference at config (d) geometry,
+    imported (recomputed chords, or its own stored spans and events) and evaluated twice
+    (the second time over the event list)."""
+    scene = S.reflectometry_scene(256, 256, 16)
+    pstr = str(tmp_path / "ref_d.pstr")
+    ref.render(scene, 3000, 7, pstr_out=pstr, sort=True, workers=WORKERS)
+    ctx.upload(scene)
+    st = ctx.load_store(pstr, materialized=materialized)
+    t = S.ParamSet(None, 0.55, 38.0)
+    F_ref = ref.evaluate(scene, pstr, None, abi.PRC_EVAL_NORMALIZE, workers=WORKERS)["images"]
+    F_t = ref.evaluate(scene, pstr, t, abi.PRC_EVAL_NORMALIZE, workers=WORKERS)["images"]
+    w = F_t - 0.9 * F_ref
+    r = ref.evaluate(scene, pstr, t, abi.PRC_EVAL_NORMALIZE | abi.PRC_EVAL_WANT_GRAD, w, workers=WORKERS)
+    for _ in range(2):
+        g = ctx.evaluate_store(scene, st, t, EvalOptions(want_grad=True, pixel_weights=w))
+        e_img = img_err(g.images, r["images"])
+        e_k = abs(g.grad_kappa - r["grad_kappa"]) / max(abs(r["grad_kappa"]), 1e-300)
+        e_g = abs(g.grad_gamma - r["grad_gamma"]) / max(abs(r["grad_gamma"]), 1e-300)
+        assert e_img <= IMG_TOL and e_k <= GRAD_TOL and e_g <= GRAD_TOL, (e_img, e_k, e_g)
+    print(f"reference-written config (d) store (materialized={materialized}): F_t {e_img:.2e}, "
+          f"d kappa {e_k:.2e}, d gamma {e_g:.2e}")
+
+
 def test_config_d_store_matches_reference(ctx, ref, tmp_path):
     """Config (d), reflectometry (phong_box walls, the central Phong sphere as the unknown,
     14 diffuse spheres, 16 inward cameras at 256^2): no medium, so after the first forward
