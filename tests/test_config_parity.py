@@ -109,22 +109,25 @@ def test_config_store_matches_reference(ctx, ref, tmp_path, cfg):
     print("; ".join(msg))
 
 
-def test_reference_written_config_a_store(ctx, ref, tmp_path):
-    """A store traced and sorted by the reference at config (a) geometry, imported."""
-    scene = CONFIGS["a"]["scene"]()
-    pstr = str(tmp_path / "ref_a.pstr")
-    ref.render(scene, 2000, 7, pstr_out=pstr, sort=True, workers=WORKERS)
+@pytest.mark.parametrize("cfg,n", [("a", 2000), ("c", 800), ("e", 600)])
+@pytest.mark.parametrize("materialized", [False, True])
+def test_reference_written_config_store(ctx, ref, tmp_path, cfg, n, materialized):
+    """A store traced and sorted by the reference at a config's geometry, imported with
+    recomputed spans or its own stored spans and events."""
+    scene = CONFIGS[cfg]["scene"]()
+    pstr = str(tmp_path / f"ref_{cfg}.pstr")
+    ref.render(scene, n, 7, pstr_out=pstr, sort=True, workers=WORKERS)
     ctx.upload(scene)
-    st = ctx.load_store(pstr)
+    st = ctx.load_store(pstr, materialized=materialized)
     assert st.sorted_flag
-    t = S.ParamSet(S.recycle_point(scene.species[0].extinction))
+    t = S.ParamSet(S.recycle_point(scene.species[scene.unknown_species()].extinction))
     F_ref = ref.evaluate(scene, pstr, None, abi.PRC_EVAL_NORMALIZE, workers=WORKERS)["images"]
     F_t = ref.evaluate(scene, pstr, t, abi.PRC_EVAL_NORMALIZE, workers=WORKERS)["images"]
     w = F_t - 0.9 * F_ref
     r = ref.evaluate(scene, pstr, t, abi.PRC_EVAL_NORMALIZE | abi.PRC_EVAL_WANT_GRAD, w, workers=WORKERS)
     g = ctx.evaluate_store(scene, st, t, EvalOptions(want_grad=True, pixel_weights=w))
     e_img, e_grad = img_err(g.images, r["images"]), grad_err(g.grad_beta, r["grad"])
-    print(f"reference-written config (a) store: F_t {e_img:.2e}, grad {e_grad:.2e}")
+    print(f"reference-written config ({cfg}) store (materialized={materialized}): F_t {e_img:.2e}, grad {e_grad:.2e}")
     assert e_img <= IMG_TOL and e_grad <= GRAD_TOL
 
 
